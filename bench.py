@@ -1,0 +1,382 @@
+"""bench.py -- headline benchmark: 2D Gaussian fits/s (15x15 px, symmetric,
+implicit alpha/beta) on N B200s vs the reference CPU fitter.
+
+Workload (BASELINE.json configs[1]): 1e6 synthetic spots per GPU,
+15x15 px, 400:40 counts, Poisson-like noise, inits from the (untimed) GPU
+initializer, exactly as PAPER.md:210-212 times the fit.  A step = one full LM
+fit of the whole batch.
+
+  value  -- fits/s with inputs resident in HBM (sf_fit_batch_device, CUDA
+            events on the launching stream, max over ranks); 900 MB of input per
+            GPU > 126 MB L2, so no L2 flush is needed between steps.
+  e2e    -- the same fit through the public API (fit_batch -> sf_fit_batch)
+            from pinned host memory: H2D + kernel + D2H inside the timed region.
+  --impl reference -- the reference CPU fitter (numpy model arithmetic of
+            pkg/src/spotfit/model.py restated in oracle/model_np.py + the App. A
+            LM loop) on all host cores, bounded sample per step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (W, H, spots per GPU, model)
+    "c2": (15, 15, 1_000_000, 3),
+    "c1": (11, 11, 10_000, 3),
+    "c3": (21, 21, 1_000_000, 4),
+    "c4": (32, 32, 1_000_000, 3),
+}
+METRIC = "2D Gaussian fits/sec (15x15 px) at 1/2/4/8 B200 vs CPU ref; % FP32/SFU roofline"
+# algorithmic work per pixel-evaluation: G-eval 67 ops (45 FP32 + 22 reduction adds),
+# T-eval 18 ops (14 + 4); one exp each.  Elliptical G-eval: 58 + 30.
+OPS_G = {3: 67, 4: 88}
+OPS_T = {3: 18, 4: 18}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+def make_workload(W, H, count, model, seed):
+    import paper_2106_02045_b200 as sf
+
+    im, _ = sf.simulate_batch(sf.SimConfig(width=W, height=H, count=count, seed=seed, model=model))
+    return im.reshape(count, W * H)
+
+
+def cpu_reference(W, H, model, images, inits, sample, workers):
+    """The reference CPU fitter on `sample` spots, all host cores -> (fits/s, seconds)."""
+    from oracle import lm
+
+    cfg = lm.LMConfig.for_grid(W, H)
+    t0 = time.perf_counter()
+    lm.fit_batch_parallel(images[:sample], inits[:sample], W, H, cfg, workers=workers)
+    dt = time.perf_counter() - t0
+    return sample / dt, dt
+
+
+def cpu_c_port(W, H, images, inits, sample, threads):
+    from oracle import lm, oracle_c
+
+    cfg = lm.LMConfig.for_grid(W, H)
+    t0 = time.perf_counter()
+    oracle_c.fit_batch(images[:sample], inits[:sample], W, H, cfg, threads=threads)
+    return sample / (time.perf_counter() - t0)
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    W, H, count, model = CONFIGS[args.config]
+    if rank != 0:
+        return 0
+    import paper_2106_02045_b200 as sf  # simulator + (host) initializer inputs only
+    from oracle import initializer as oinit
+
+    cores = len(os.sched_getaffinity(0))
+    sample = args.ref_sample or max(2000, 500 * cores)
+    images = make_workload(W, H, sample, model, seed=2021)
+    inits, _ = oinit.estimate_initial_batch(images, W, H, 0.3, float(max(W, H)), model)
+    for _ in range(args.warmup):
+        cpu_reference(W, H, model, images, inits, min(sample, 64 * cores), cores)
+    times = []
+    for _ in range(args.steps):
+        _, dt = cpu_reference(W, H, model, images, inits, sample, cores)
+        times.append(dt)
+    total = float(np.sum(times))
+    value = sample * args.steps / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "fits/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64",
+        "data": "synthetic (SPEC.md:316-368 simulator, 400:40 counts)",
+        "config": {"workload": f"{args.config}: {W}x{H} symmetric, bounded sample of {sample} spots per step",
+                   "spots_per_step": sample, "cores": cores},
+        "cpu_baseline": {"value": value, "unit": "fits/s", "cores": cores, "kind": "port",
+                         "sample": f"{sample} spots of the {W}x{H} workload per step, {args.steps} steps"},
+        "e2e": {"value": value, "unit": "fits/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def run_ours(args):
+    import torch
+
+    import paper_2106_02045_b200 as sf
+    from paper_2106_02045_b200 import _lib
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+    W, H, count, model = CONFIGS[args.config]
+    if args.count:
+        count = args.count
+    N = W * H
+    grid = sf.PixelGrid(W, H)
+    cfg = sf.FitConfig()
+    ccfg = cfg.to_c(grid, model)
+    L = _lib.lib()
+
+    # ---- synthetic inputs (untimed): simulator -> HBM; GPU initializer (untimed)
+    t0 = time.perf_counter()
+    images = make_workload(W, H, count, model, seed=1000 + rank)
+    d_img = torch.from_numpy(images).to(dev)
+    d_ini = sf.batch_engine.estimate_initial_device(d_img, grid, model, cfg)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    d_par = torch.empty((count, model), dtype=torch.float32, device=dev)
+    d_f = torch.empty((3, count), dtype=torch.float32, device=dev)
+    d_u8 = torch.empty((2, count), dtype=torch.uint8, device=dev)
+    d_ev = torch.zeros(3, dtype=torch.int64, device=dev)
+    stream = torch.cuda.Stream(dev)
+
+    def step():
+        rc = L.sf_fit_batch_device(d_img.data_ptr(), W, H, count, d_ini.data_ptr(), ctypes_byref(ccfg),
+                                   d_par.data_ptr(), d_f[0].data_ptr(), d_f[1].data_ptr(), d_f[2].data_ptr(),
+                                   d_u8[0].data_ptr(), d_u8[1].data_ptr(), d_ev.data_ptr(), stream.cuda_stream)
+        _lib.check(rc)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+    stream.synchronize()
+    d_ev.zero_()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        stream.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    evs = d_ev.cpu().tolist()
+    ms_max = ms
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_max = float(t.item())
+    fits = count * world * args.steps
+    value = fits / (ms_max * 1e-3)
+
+    # ---- end to end through the public API from pinned host memory
+    pin_img = torch.from_numpy(images).pin_memory()
+    pin_ini = d_ini.cpu().pin_memory()
+    outs = sf.BatchResult(*[torch.empty(s, dtype=d).pin_memory().numpy() for s, d in [
+        ((count, model), torch.float32), (count, torch.float32), (count, torch.float32), (count, torch.float32),
+        (count, torch.uint8), (count, torch.uint8)]])
+    engine = "implicit3" if model == 3 else "elliptical"
+    for _ in range(max(1, args.warmup)):
+        sf.fit_batch(pin_img.numpy(), pin_ini.numpy(), config=cfg, engine=engine, grid=grid, out=outs)
+    barrier()
+    e2e_steps = max(3, args.steps // 2)
+    chunks = 0
+    t_host = []
+    for _ in range(e2e_steps):
+        barrier()
+        a = time.perf_counter()
+        r = sf.fit_batch(pin_img.numpy(), pin_ini.numpy(), config=cfg, engine=engine, grid=grid, out=outs)
+        t_host.append(time.perf_counter() - a)
+        chunks = r.stats["n_chunks"]
+    e2e_s = float(np.sum(t_host))
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = count * world * e2e_steps / e2e_s
+
+    # ---- parity on a sample (GPU vs C oracle, bitwise) and CPU baselines (rank 0)
+    result = {}
+    if rank == 0:
+        from oracle import lm, oracle_c
+
+        par = d_par.cpu().numpy()
+        f = d_f.cpu().numpy()
+        u8 = d_u8.cpu().numpy()
+        ini = d_ini.cpu().numpy()
+        sample_idx = np.linspace(0, count - 1, min(count, args.parity_sample)).astype(np.int64)
+        ref = oracle_c.fit_batch(images[sample_idx], ini[sample_idx], W, H, lm.LMConfig.for_grid(W, H))
+        same = np.ones(len(sample_idx), bool)
+        for k, got in (("params", par[sample_idx]), ("alpha", f[0][sample_idx]), ("beta", f[1][sample_idx]),
+                       ("nchi2", f[2][sample_idx]), ("status", u8[0][sample_idx]),
+                       ("iterations", u8[1][sample_idx])):
+            eq = (np.asarray(got).view(np.uint8).reshape(len(sample_idx), -1) ==
+                  np.asarray(ref[k]).view(np.uint8).reshape(len(sample_idx), -1)).all(axis=1)
+            same &= eq
+        result["parity"] = {"sample": int(len(sample_idx)), "bitwise_identical_frac": float(same.mean()),
+                            "state_identical_frac": float((u8[0][sample_idx] == ref["status"]).mean()),
+                            "checker": "oracle/spotfit_oracle.c (pinned to reference model.py fixtures)"}
+        cores = len(os.sched_getaffinity(0))
+        samp = args.ref_sample or max(2000, 500 * cores)
+        cpu_v, cpu_dt = cpu_reference(W, H, model, images, ini, samp, cores)
+        c_v = cpu_c_port(W, H, images, ini, min(count, 20 * samp), cores)
+        result["cpu_baseline"] = {"value": cpu_v, "unit": "fits/s", "cores": cores, "kind": "port",
+                                  "sample": f"{samp} spots of this workload through oracle/lm.py over "
+                                            f"oracle/model_np.py (reference numpy arithmetic), {cpu_dt:.1f} s"}
+        result["cpu_c_port"] = {"value": c_v, "unit": "fits/s", "cores": cores,
+                                "note": "bit-exact C restatement (oracle/spotfit_oracle.c), stronger CPU comparator"}
+
+    # ---- roofline: algorithmic FP32 ops per launch / kernel time
+    n_g, n_t, n_k = (v / max(1, args.steps) for v in evs)  # per launch (= per step)
+    ops = N * (OPS_G[model] * n_g + OPS_T[model] * n_t)
+    exps = N * (n_g + n_t)
+    launch_s = ms * 1e-3 / args.steps
+    peaks = load_peaks()
+    clks = clk.summary()
+    sm_max = clks.get("sm_max_mhz") or peaks.get("sm_max_mhz") or 1965.0
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    fp32_peak = sms * 128 * sm_max * 1e6
+    sfu_peak = sms * 16 * sm_max * 1e6
+    achieved = ops / launch_s
+    hbm_bytes = count * (4 * N + 4 * model) + count * (4 * model + 12 + 2)
+    f2f_per_pix = {3: 22, 4: 30}[model]
+    f2f_ops = N * n_k * f2f_per_pix
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "fits/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32 (per-pixel) / f64 (sums)",
+            "data": "synthetic (simulator SPEC.md:316-368, 400:40 counts, seeded), inits from the untimed GPU initializer",
+            "config": {"workload": f"{args.config}: {count} {'symmetric' if model == 3 else 'elliptical'} spots/GPU, "
+                                   f"{W}x{H} px, max 20 LM iterations", "spots_per_gpu": count, "W": W, "H": H,
+                       "model": model, "parallelism": f"independent shards x{world}",
+                       "l2": f"inputs {count * N * 4 / 1e6:.0f} MB/GPU > 126 MB L2 (no flush needed)"},
+            "roofline": {"bound": "fp32", "achieved": achieved / 1e12, "peak": fp32_peak / 1e12, "unit": "TOP/s",
+                         "frac": achieved / fp32_peak, "traffic": None,
+                         "ops_per_fit": ops / count, "def": "SURVEY 8d: N*(67*n_G + 18*n_T) algorithmic ops per fit; "
+                                                            "peak = SMs*128*sm_max_mhz (FP32 lanes)",
+                         "sfu": {"achieved": exps / launch_s / 1e12, "peak": sfu_peak / 1e12,
+                                 "frac": exps / launch_s / sfu_peak},
+                         "hbm": {"achieved": hbm_bytes / launch_s / 1e9, "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
+                                 "frac": (hbm_bytes / launch_s / 1e9) / peaks["hbm_gbs"] if peaks.get("hbm_gbs") else None,
+                                 "peak_source": "MEASURED_PEAKS.json (measured)"},
+                         "f2f": {"achieved": f2f_ops / launch_s / 1e12, "peak": sms * 16 * sm_max * 1e6 / 1e12,
+                                 "frac": (f2f_ops / launch_s) / (sms * 16 * sm_max * 1e6),
+                                 "def": "F2F.F64.F32 widenings the bit-exact f64 sums need (16/clk/SM, measured)"}},
+            "e2e": {"value": e2e_value, "unit": "fits/s", "h2d_bytes_per_step": count * (N + model) * 4,
+                    "d2h_bytes_per_step": count * (model * 4 + 3 * 4 + 2), "steps": e2e_steps,
+                    "path": "fit_batch -> sf_fit_batch, pinned host buffers, chunked H2D/kernel/D2H",
+                    "chunks_per_step": chunks},
+            "gpu_launches": args.steps,
+            "evals_per_fit": {"n_G": n_g / count, "n_T": n_t / count, "kernel": n_k / count},
+            "clocks": clks,
+            "setup_s": setup_s,
+        }
+        line.update(result)
+        print(json.dumps(line))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def ctypes_byref(x):
+    import ctypes
+
+    return ctypes.byref(x)
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--count", type=int, default=0, help="override spots per GPU")
+    ap.add_argument("--ref-sample", type=int, default=0)
+    ap.add_argument("--parity-sample", type=int, default=20000)
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,173 @@
+/*
+ * spotfit.h -- C-ABI of the B200-native implicit-amplitude LM spot fitter.
+ *
+ * Drop-in boundary for the reference's batch fit path.  The
+ * reference (arXiv 2106.02045, /root/reference) exposes this path as Python:
+ *
+ *   fit_batch(BatchRequest{images, inits|None, config, engine, workers})
+ *       -> [FitResult]
+ *   fit_single(image, init, config) -> FitResult
+ *   the model arithmetic spotfit.model.*                   pkg/src/spotfit/model.py:154-315
+ *   estimate_initial(image, bounds)
+ *   simulate_spot / simulate_batch
+ *
+ * Each entry point below cites the reference interface it replaces.  Plain
+ * pointers and sizes only; no torch types.  All functions are reentrant and
+ * blocking; the library keeps per-device streams and scratch memory in an
+ * internal context guarded by a mutex per device.  A non-zero return code is
+ * reserved for argument, CUDA or launch failures (message: sf_last_error());
+ * per-spot failures are reported in out_status.
+ *
+ * Result layout per spot: shape params
+ * (x, y, sigma) or (x, y, sigma_x, sigma_y), alpha, beta, normalised chi^2,
+ * status byte (StopReason in the low 3 bits + flags), iterations used.
+ */
+#ifndef SPOTFIT_H
+#define SPOTFIT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SF_ABI_VERSION 1
+
+/* StopReason in the low 3 bits of the status byte */
+#define SF_STOP_MAX_ERROR 0
+#define SF_STOP_MIN_DELTA 1
+#define SF_STOP_MIN_STEP 2
+#define SF_STOP_NOT_CONVERGED 3
+#define SF_STOP_MAX_ITERATIONS 4
+#define SF_FLAG_INVALID 0x40 /* InvalidInput: non-finite pixel or init */
+#define SF_FLAG_NOIMP 0x80   /* no chi^2 decrease after the lambda retries (SURVEY App. A [A2]) */
+
+/* model selector */
+#define SF_MODEL_SYMMETRIC 3  /* (x, y, sigma)            model.py:100-115 */
+#define SF_MODEL_ELLIPTICAL 4 /* (x, y, sigma_x, sigma_y) SURVEY App. B.5, no reference */
+
+/* FitConfig + ParameterBounds (defaults) */
+typedef struct sf_config {
+  int32_t model;          /* SF_MODEL_SYMMETRIC | SF_MODEL_ELLIPTICAL */
+  int32_t max_iterations; /* 1..255, default 20 */
+  double max_error;       /* chi^2 early stop, default 0 = disabled */
+  double min_delta;       /* relative chi^2 improvement, default 1e-6 */
+  double min_step;        /* relative parameter change, default 1e-4 */
+  double lambda_init;     /* 0.01 */
+  double lambda_up;       /* 10 */
+  double lambda_down;     /* 10 */
+  double lambda_max;      /* 1e4 */
+  double margin_x;        /* centre may leave the grid by this much, default W/2 */
+  double margin_y;        /* default H/2 */
+  double sigma_min;       /* default 0.3 */
+  double sigma_max;       /* default max(W, H) */
+} sf_config;
+
+/* Evaluation counters and timings of one sf_fit_batch call. */
+typedef struct sf_stats {
+  uint64_t n_gradient_evals; /* reference-accounted G-evals (= sum of iterations) */
+  uint64_t n_trial_evals;    /* reference-accounted T-evals (trial chi^2 evaluations) */
+  uint64_t n_kernel_evals;   /* full evaluations the fused kernel executed */
+  double h2d_ms, kernel_ms, d2h_ms, total_ms; /* device-event times (summed over chunks / devices) */
+  int32_t n_devices;
+  int32_t n_chunks;
+} sf_stats;
+
+/*
+ * sf_fit_batch -- replaces fit_batch / per-spot fit_single
+ * (SPEC.md:209).  images: [count][H][W] f32 row-major (SpotImage values,
+ * model.py:70-93); inits: [count][P] f32 (ShapeParams; estimate_initial output).
+ * Pointers may be host (pageable or pinned) or device memory of devices[0];
+ * the library detects which.  Host inputs are streamed in chunks over copy/compute
+ * streams; with n_devices > 1 the batch is split into contiguous shards, one
+ * host thread per device, results written into disjoint slices.
+ * out_params: [count][P]; out_alpha/out_beta/out_nchi2: [count]; out_status,
+ * out_iters: [count] bytes.  stats may be NULL.
+ */
+int sf_fit_batch(const float* images, int32_t width, int32_t height, int64_t count, const float* inits,
+                 const sf_config* cfg, float* out_params, float* out_alpha, float* out_beta, float* out_nchi2,
+                 uint8_t* out_status, uint8_t* out_iters, const int32_t* devices, int32_t n_devices,
+                 sf_stats* stats);
+
+/*
+ * sf_fit_batch_device -- the same fit with every pointer in device memory of
+ * the current device, launched on `stream` (cudaStream_t, 0 = legacy default),
+ * asynchronous.  Used by bench.py for the HBM-resident measurement and by
+ * callers that already hold spots on the GPU.  evals_out: device u64[3]
+ * accumulating (G-evals, T-evals, kernel evals) or NULL.
+ */
+int sf_fit_batch_device(const float* d_images, int32_t width, int32_t height, int64_t count, const float* d_inits,
+                        const sf_config* cfg, float* d_params, float* d_alpha, float* d_beta, float* d_nchi2,
+                        uint8_t* d_status, uint8_t* d_iters, uint64_t* d_evals, void* stream);
+
+/*
+ * sf_eval_batch_device -- model-level evaluation at given shape parameters
+ * (one evaluation per spot, no LM): replaces the spotfit.model call chain
+ * profile_and_gradient -> alpha_beta -> chi_squared -> gradient_sums ->
+ * coefficient_gradients -> chi_gradient (model.py:180-315) plus the normal
+ * matrix.  out: [count] records of sf_eval_record below.
+ */
+typedef struct sf_eval_record {
+  int32_t singular; /* SingularProfile raised (model.py:228-231) */
+  float alpha, beta, chi;
+  double F, G, FF, FG, denom;
+  double dF[4], dFF[4], dFG[4], gamma[4], dalpha[4], dbeta[4];
+  double rhs[4];  /* sum r*d_j = -grad_j/2 (model.py:314) */
+  double jtj[10]; /* upper-packed normal matrix */
+} sf_eval_record;
+
+int sf_eval_batch_device(const float* d_images, int32_t width, int32_t height, int64_t count, int32_t model,
+                         const float* d_params, sf_eval_record* d_out, void* stream);
+
+/*
+ * sf_estimate_initial_device -- replaces estimate_initial (SPEC.md:286-290,
+ * PAPER.md:212) for a whole batch on the GPU: 3x3 truncated moving average,
+ * argmax -> centre, min -> beta, max-beta -> alpha, sigma = sqrt(M/pi) clamped.
+ * out_inits: [count][model] f32 (elliptical: sigma_x = sigma_y); out_amps:
+ * [count][2] (alpha, beta) or NULL.  Asynchronous on `stream`.
+ */
+int sf_estimate_initial_device(const float* d_images, int32_t width, int32_t height, int64_t count, int32_t model,
+                               double sigma_min, double sigma_max, float* d_inits, float* d_amps, void* stream);
+
+/*
+ * sf_simulate_host -- replaces simulate_batch: synthetic
+ * spots with a counter-based RNG keyed by (seed, index), so any
+ * index can be regenerated alone.  images: [count][H][W]; truth: [count][P+2]
+ * (shape params, alpha, beta).  Runs on host threads (threads <= 0: all cores).
+ */
+typedef struct sf_sim_config {
+  int32_t model;      /* 3 or 4 */
+  double n_signal;    /* 400 */
+  double n_background;/* 40 (per image; beta = n_background / (W*H)) */
+  double sigma_lo, sigma_hi; /* [1, 2] */
+  double spread;      /* centre std in px; <= 0 means S/20 per axis */
+  int32_t noise;      /* 1: N(0, lambda) noise, rounded, clamped at 0 */
+  int32_t rounding;   /* 1: round half away from zero */
+  uint64_t seed;
+} sf_sim_config;
+
+int sf_simulate_host(const sf_sim_config* cfg, int32_t width, int32_t height, int64_t first_index, int64_t count,
+                     float* images, float* truth, int32_t threads);
+
+/* pinned host allocations (so that callers' buffers DMA directly) */
+void* sf_host_alloc(size_t bytes);
+void sf_host_free(void* p);
+
+/*
+ * sf_lane_geometry -- diagnostic: how a W x H spot maps onto chain lanes
+ * (numpy's pairwise-sum tree).  Writes slots (1..16) and, per
+ * lane (8*slots entries, up to 128), the chain-pixel count nc, tail-pixel count
+ * nt, first chain pixel base and first tail pixel tbase.  Host-only.
+ */
+int sf_lane_geometry(int32_t width, int32_t height, int32_t* slots, int32_t* ppl, int16_t* nc, int16_t* nt,
+                     int16_t* base, int16_t* tbase);
+
+int sf_device_count(void);
+const char* sf_last_error(void);
+int sf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPOTFIT_H */

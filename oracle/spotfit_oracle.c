@@ -1,0 +1,409 @@
+/*
+ * spotfit_oracle.c -- CPU restatement of the reference fit path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  This file is the checker for the CUDA product
+ * path: only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load it.  The product (paper_2106_02045_b200/)
+ * never links or calls it.
+ *
+ * What is restated, and from where (all citations into /root/reference):
+ *   npexp_f32        numpy 2.3.5 float32 exp (AVX512F/AVX2 simd_exp_f32), the
+ *                    np.exp called at pkg/src/spotfit/model.py:177,193.
+ *                    Constants / op order: SURVEY.md App. B.2 (third-party
+ *                    dependency numpy>=1.24, pyproject.toml:12).  Pinned by
+ *                    tests/test_oracle_numerics.py against this host's np.exp.
+ *   pw_sum           numpy float64 pairwise add-reduce of a float32 array
+ *                    (x.sum(dtype=np.float64), model.py:222-225,250,263-265,314)
+ *                    SURVEY.md App. B.3.  Pinned against np.sum in tests.
+ *   sf_oracle_eval   model.py:154-315 (profile_and_gradient, alpha_beta,
+ *                    chi_squared, gradient_sums, coefficient_gradients,
+ *                    chi_gradient) + the normal matrix of SPEC.md:173-176.
+ *                    Pinned bit-for-bit against the reference model.py via
+ *                    tests/golden/*.npz (tests/golden/make_golden.py).
+ *   sf_oracle_fit    LM state machine of PAPER.md:126-180 / SPEC.md:209-262 as
+ *                    pinned in SURVEY.md App. A (and DESIGN.md section 3).
+ *   elliptical (P=4) SURVEY.md App. B.5 -- no reference exists (SPEC.md:152
+ *                    lists it as a non-goal): parity for P=4 is unpinned.
+ *
+ * Build: oracle/Makefile  (-O2 -ffp-contract=off: no FMA contraction).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <float.h>
+#include <pthread.h>
+
+#include "spotfit_oracle.h"
+
+/* ------------------------------------------------------------------ */
+/* numpy float32 exp                                 */
+/* ------------------------------------------------------------------ */
+static float ldexp_single_round(float r, int q) {
+  /* r in [0.7, 1.42]; one rounding of r * 2^q, denormals kept */
+  if (q >= -126 && q <= 127) {
+    union { uint32_t u; float f; } s; s.u = (uint32_t)(q + 127) << 23;
+    return r * s.f;
+  }
+  if (q > 127) {                       /* r*2*2^127: first product exact */
+    union { uint32_t u; float f; } s; s.u = (uint32_t)(127 + 127) << 23;
+    return (r * 2.0f) * s.f;
+  }
+  { /* q < -126: r*2^(q+64) exact (normal), then *2^-64 rounds once */
+    union { uint32_t u; float f; } s; s.u = (uint32_t)(q + 64 + 127) << 23;
+    union { uint32_t u; float f; } t; t.u = (uint32_t)(-64 + 127) << 23;
+    return (r * s.f) * t.f;
+  }
+}
+
+float npexp_f32(float x) {
+  if (x != x) return x;
+  if (x >= 88.72283935546875f) return INFINITY;
+  if (x <= -103.97208404541015625f) return 0.0f;
+  volatile float t = x * 1.442695040888963407359924681001892137f; /* rounded mul */
+  float q = (t + 0x1.8p23f) - 0x1.8p23f;                            /* RNE to int */
+  float y = fmaf(q, -6.93145752e-1f, x);
+  y = fmaf(q, -1.42860677e-6f, y);
+  float n = fmaf(5.082762527590693718096e-4f, y, 6.757896990527504603057e-3f);
+  n = fmaf(n, y, 5.114512081637298353406e-2f);
+  n = fmaf(n, y, 2.473615434895520810817e-1f);
+  n = fmaf(n, y, 7.257664613233124478488e-1f);
+  n = fmaf(n, y, 9.999999999980870924916e-1f);
+  float d = fmaf(2.159509375685829852307e-2f, y, -2.742335390411667452936e-1f);
+  d = fmaf(d, y, 1.0f);
+  float r = n / d;
+  return ldexp_single_round(r, (int)q);
+}
+
+void npexp_f32_array(const float* x, float* y, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) y[i] = npexp_f32(x[i]);
+}
+
+/* ------------------------------------------------------------------ */
+/* numpy pairwise float64 sum of float32             */
+/* ------------------------------------------------------------------ */
+static double pw_rec(const float* a, int n) {
+  if (n < 8) {
+    double res = 0.0;
+    for (int i = 0; i < n; ++i) res += (double)a[i];
+    return res;
+  }
+  if (n <= 128) {
+    double r[8];
+    for (int k = 0; k < 8; ++k) r[k] = (double)a[k];
+    int i;
+    for (i = 8; i < n - (n % 8); i += 8)
+      for (int k = 0; k < 8; ++k) r[k] += (double)a[i + k];
+    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; ++i) res += (double)a[i];
+    return res;
+  }
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return pw_rec(a, n2) + pw_rec(a + n2, n - n2);
+}
+
+double pw_sum(const float* a, int n) { return 0.0 + pw_rec(a, n); }
+
+/* ------------------------------------------------------------------ */
+/* model evaluation (model.py:154-315)                */
+/* ------------------------------------------------------------------ */
+#define DENOM_GUARD 1e-12 /* model.py:28 */
+
+int sf_oracle_eval(const float* g, int W, int H, int P, const float* p, sf_oracle_eval_t* e) {
+  const int N = W * H;
+  float f[SF_ORACLE_MAXPIX], fg[4][SF_ORACLE_MAXPIX], t[SF_ORACLE_MAXPIX];
+  float d[4][SF_ORACLE_MAXPIX], r[SF_ORACLE_MAXPIX];
+  memset(e, 0, sizeof(*e));
+  if (N < 1 || N > SF_ORACLE_MAXPIX || (P != 3 && P != 4)) return -1;
+  /* _scaled_offsets (model.py:154-165) / profile_and_gradient (model.py:180-199) */
+  if (P == 3) {
+    const float x0 = p[0], y0 = p[1], inv = 1.0f / p[2];
+    for (int i = 0; i < N; ++i) {
+      const float xi = (float)(i % W), yi = (float)(i / W);
+      const float u = (xi - x0) * inv, v = (yi - y0) * inv;
+      const float uu = u * u, vv = v * v;
+      const float q = uu + vv;
+      f[i] = npexp_f32(-0.5f * q);
+      const float fs = f[i] * inv;
+      fg[0][i] = u * fs; fg[1][i] = v * fs; fg[2][i] = q * fs;
+    }
+  } else { /* SURVEY App. B.5 (no reference) */
+    const float x0 = p[0], y0 = p[1], ix = 1.0f / p[2], iy = 1.0f / p[3];
+    for (int i = 0; i < N; ++i) {
+      const float xi = (float)(i % W), yi = (float)(i / W);
+      const float u = (xi - x0) * ix, v = (yi - y0) * iy;
+      const float uu = u * u, vv = v * v;
+      const float q = uu + vv;
+      f[i] = npexp_f32(-0.5f * q);
+      const float fx = f[i] * ix, fy = f[i] * iy;
+      fg[0][i] = u * fx; fg[1][i] = v * fy;
+      fg[2][i] = u * fg[0][i]; fg[3][i] = v * fg[1][i];
+    }
+  }
+  const double n = (double)N;
+  /* alpha_beta (model.py:207-234) */
+  e->F = pw_sum(f, N);
+  e->G = pw_sum(g, N);
+  for (int i = 0; i < N; ++i) t[i] = f[i] * f[i];
+  e->FF = pw_sum(t, N);
+  for (int i = 0; i < N; ++i) t[i] = f[i] * g[i];
+  e->FG = pw_sum(t, N);
+  e->denom = n * e->FF - e->F * e->F;
+  if (e->denom <= DENOM_GUARD * n * e->FF) { e->singular = 1; return 0; }
+  const double alpha = (n * e->FG - e->F * e->G) / e->denom;
+  const double beta = (e->G * e->FF - e->F * e->FG) / e->denom;
+  e->alpha = (float)alpha; e->beta = (float)beta;
+  /* chi_squared (model.py:237-250) */
+  const float a32 = e->alpha, b32 = e->beta;
+  for (int i = 0; i < N; ++i) { const float h = a32 * f[i] + b32; r[i] = g[i] - h; t[i] = r[i] * r[i]; }
+  e->chi = (float)pw_sum(t, N);
+  /* gradient_sums (model.py:253-267) */
+  for (int j = 0; j < P; ++j) {
+    e->dF[j] = pw_sum(fg[j], N);
+    for (int i = 0; i < N; ++i) t[i] = f[i] * fg[j][i];
+    e->dFF[j] = 2.0 * pw_sum(t, N);
+    for (int i = 0; i < N; ++i) t[i] = g[i] * fg[j][i];
+    e->dFG[j] = pw_sum(t, N);
+    e->gamma[j] = n * e->dFF[j] - 2.0 * e->F * e->dF[j];
+  }
+  /* coefficient_gradients (model.py:270-288) */
+  for (int j = 0; j < P; ++j) {
+    e->dalpha[j] = (n * e->dFG[j] - e->G * e->dF[j] - (double)a32 * e->gamma[j]) / e->denom;
+    e->dbeta[j] = (e->G * e->dFF[j] - e->FG * e->dF[j] - e->F * e->dFG[j] - (double)b32 * e->gamma[j]) / e->denom;
+  }
+  /* chi_gradient (model.py:291-315): d_ij, rhs_j = sum r*d_j = -grad_j/2 */
+  for (int j = 0; j < P; ++j) {
+    const float da = (float)e->dalpha[j], db = (float)e->dbeta[j];
+    for (int i = 0; i < N; ++i) {
+      const float t1 = da * f[i], t2 = a32 * fg[j][i];
+      d[j][i] = (t1 + t2) + db;
+    }
+    for (int i = 0; i < N; ++i) t[i] = r[i] * d[j][i];
+    e->rhs[j] = pw_sum(t, N);
+  }
+  /* normal matrix: f32 products, f64 pairwise sums */
+  int m = 0;
+  for (int j = 0; j < P; ++j)
+    for (int k = j; k < P; ++k) {
+      for (int i = 0; i < N; ++i) t[i] = d[j][i] * d[k][i];
+      e->jtj[m++] = pw_sum(t, N);
+    }
+  return 0;
+}
+
+/* ------------------------------------------------------------------ */
+/* damped LDL^T solve (pinned in DESIGN.md 3.2)       */
+/* ------------------------------------------------------------------ */
+static inline int sym_idx(int P, int i, int j) { /* upper-packed row-major */
+  if (i > j) { int t = i; i = j; j = t; }
+  return i * P - (i * (i - 1)) / 2 + (j - i);
+}
+
+int sf_oracle_solve(int P, const double* jtj, const double* rhs, double lam, double* delta) {
+  double A[4][4], L[4][4], C[4][4], D[4], z[4];
+  for (int i = 0; i < P; ++i)
+    for (int j = 0; j < P; ++j) A[i][j] = jtj[sym_idx(P, i, j)];
+  for (int i = 0; i < P; ++i) A[i][i] = A[i][i] + lam * A[i][i];
+  for (int i = 0; i < P; ++i) {
+    for (int j = 0; j < i; ++j) {
+      double s = A[i][j];
+      for (int k = 0; k < j; ++k) s = s - C[i][k] * L[j][k];
+      C[i][j] = s;
+      L[i][j] = s / D[j];
+    }
+    double s = A[i][i];
+    for (int k = 0; k < i; ++k) s = s - C[i][k] * L[i][k];
+    D[i] = s;
+    if (!(D[i] > 0.0)) return 0;
+  }
+  double det = D[0], dprod = A[0][0];
+  for (int i = 1; i < P; ++i) { det = det * D[i]; dprod = dprod * A[i][i]; }
+  if (!(det > SF_STEP_GUARD * dprod)) return 0;
+  for (int i = 0; i < P; ++i) {
+    double s = rhs[i];
+    for (int k = 0; k < i; ++k) s = s - L[i][k] * z[k];
+    z[i] = s;
+  }
+  for (int i = 0; i < P; ++i) z[i] = z[i] / D[i];
+  for (int i = P - 1; i >= 0; --i) {
+    double s = z[i];
+    for (int k = i + 1; k < P; ++k) s = s - L[k][i] * delta[k];
+    delta[i] = s;
+  }
+  return 1;
+}
+
+/* ------------------------------------------------------------------ */
+/* limit and the LM state machine    */
+/* ------------------------------------------------------------------ */
+static inline double clampd(double v, double lo, double hi) {
+  return v < lo ? lo : (v > hi ? hi : v); /* NaN passes through */
+}
+
+static void limit_params(int P, int W, int H, const sf_oracle_config_t* c, const double* v, float* out) {
+  out[0] = (float)clampd(v[0], -c->margin_x, (double)(W - 1) + c->margin_x);
+  out[1] = (float)clampd(v[1], -c->margin_y, (double)(H - 1) + c->margin_y);
+  for (int j = 2; j < P; ++j) out[j] = (float)clampd(v[j], c->sigma_min, c->sigma_max);
+}
+
+static void set_result(int P, int N, const float* p, const sf_oracle_eval_t* e, sf_oracle_result_t* res) {
+  for (int j = 0; j < P; ++j) res->params[j] = p[j];
+  if (e->singular) {
+    res->alpha = NAN; res->beta = NAN; res->nchi2 = NAN;
+  } else {
+    res->alpha = e->alpha; res->beta = e->beta;
+    res->nchi2 = N > 5 ? (float)((double)e->chi / (double)(N - 5)) : e->chi;
+  }
+}
+
+int sf_oracle_fit(const float* g, int W, int H, int P, const float* init, const sf_oracle_config_t* c,
+                  sf_oracle_result_t* res) {
+  const int N = W * H;
+  memset(res, 0, sizeof(*res));
+  if (N < 1 || N > SF_ORACLE_MAXPIX || (P != 3 && P != 4)) return -1;
+  /* InvalidInput: per-image status, not a batch failure */
+  int bad = 0;
+  for (int i = 0; i < N; ++i) bad |= !isfinite(g[i]);
+  for (int j = 0; j < P; ++j) bad |= !isfinite(init[j]);
+  if (bad) {
+    for (int j = 0; j < P; ++j) res->params[j] = init[j];
+    res->alpha = res->beta = res->nchi2 = NAN;
+    res->status = SF_STOP_NOT_CONVERGED | SF_FLAG_INVALID;
+    res->iterations = 0;
+    return 0;
+  }
+  float p[4], best[4], trial[4];
+  double v[4], delta[4], thr[4];
+  sf_oracle_eval_t Eb, Et;
+  {
+    for (int j = 0; j < P; ++j) v[j] = (double)init[j];
+    limit_params(P, W, H, c, v, p);
+  }
+  double lam = c->lambda_init;
+  int it = 0, stop = SF_STOP_MAX_ITERATIONS, noimp = 0;
+  const sf_oracle_eval_t* final_e = NULL;
+  const float* final_p = p;
+  int have_trial = 0;
+  while (it < c->max_iterations) {
+    it += 1;
+    sf_oracle_eval(g, W, H, P, p, &Eb);                 /* G-eval */
+    if (Eb.singular || !isfinite(Eb.chi)) { stop = SF_STOP_NOT_CONVERGED; final_e = &Eb; final_p = p; break; }
+    if ((double)Eb.chi < c->max_error) { stop = SF_STOP_MAX_ERROR; final_e = &Eb; final_p = p; break; }
+    const float chib = Eb.chi;
+    for (int j = 0; j < P; ++j) {
+      best[j] = p[j];
+      const double a = fabs((double)best[j]);
+      thr[j] = c->min_step * (a > 1.0 ? a : 1.0);
+    }
+    float chit;
+    int small;
+    /* one trial: solve -> limit -> T-eval; StepFailed => chit=+inf, not small */
+#define SF_TRIAL()                                                                  \
+    do {                                                                            \
+      if (sf_oracle_solve(P, Eb.jtj, Eb.rhs, lam, delta)) {                         \
+        for (int j = 0; j < P; ++j) v[j] = (double)best[j] + delta[j];              \
+        limit_params(P, W, H, c, v, trial);                                         \
+        sf_oracle_eval(g, W, H, P, trial, &Et);                                     \
+        have_trial = 1;                                                             \
+        chit = Et.singular ? NAN : Et.chi;                                          \
+        small = 1;                                                                  \
+        for (int j = 0; j < P; ++j) small &= fabs(delta[j]) < thr[j];               \
+      } else {                                                                      \
+        chit = INFINITY; small = 0; have_trial = 0;                                 \
+      }                                                                             \
+    } while (0)
+    SF_TRIAL();
+    if (chib > chit) lam = lam / c->lambda_down;
+    while (!small && chib < chit && lam < c->lambda_max) {
+      lam = lam * c->lambda_up;
+      SF_TRIAL();
+    }
+#undef SF_TRIAL
+    if (isnan(chit) || (chib < chit && lam >= c->lambda_max)) {
+      stop = SF_STOP_NOT_CONVERGED; final_e = &Eb; final_p = best; break;
+    }
+    if (chib < chit) { stop = SF_STOP_MIN_DELTA; noimp = 1; final_e = &Eb; final_p = best; break; } /* [A2] */
+    /* accepted: current := trial */
+    for (int j = 0; j < P; ++j) p[j] = trial[j];
+    (void)have_trial;
+    final_e = &Et; final_p = p;
+    if ((double)chit < c->max_error) { stop = SF_STOP_MAX_ERROR; break; }
+    if ((double)chib * (1.0 - c->min_delta) < (double)chit) { stop = SF_STOP_MIN_DELTA; break; } /* :172 */
+    if (small) { stop = SF_STOP_MIN_STEP; break; }                                      /* :174 */
+  }
+  set_result(P, N, final_p, final_e, res);
+  res->status = (uint8_t)(stop | (noimp ? SF_FLAG_NOIMP : 0));
+  res->iterations = (uint8_t)it;
+  return 0;
+}
+
+/* batch drivers: contiguous chunks per pthread */
+typedef struct {
+  const float* images; int W, H, P; int64_t lo, hi; const float* inits; const sf_oracle_config_t* c;
+  const float* params; sf_oracle_eval_t* eout;
+  float *out_params, *out_alpha, *out_beta, *out_nchi2; uint8_t *out_status, *out_iters; int err;
+} sf_chunk_t;
+
+static void* fit_chunk(void* arg) {
+  sf_chunk_t* k = (sf_chunk_t*)arg;
+  const int N = k->W * k->H, P = k->P;
+  for (int64_t s = k->lo; s < k->hi; ++s) {
+    sf_oracle_result_t r;
+    k->err |= sf_oracle_fit(k->images + s * N, k->W, k->H, P, k->inits + s * P, k->c, &r);
+    for (int j = 0; j < P; ++j) k->out_params[s * P + j] = r.params[j];
+    k->out_alpha[s] = r.alpha; k->out_beta[s] = r.beta; k->out_nchi2[s] = r.nchi2;
+    k->out_status[s] = r.status; k->out_iters[s] = r.iterations;
+  }
+  return NULL;
+}
+
+static void* eval_chunk(void* arg) {
+  sf_chunk_t* k = (sf_chunk_t*)arg;
+  const int N = k->W * k->H, P = k->P;
+  for (int64_t s = k->lo; s < k->hi; ++s)
+    k->err |= sf_oracle_eval(k->images + s * N, k->W, k->H, P, k->params + s * P, k->eout + s);
+  return NULL;
+}
+
+static int run_chunks(sf_chunk_t* proto, int64_t count, int threads, void* (*fn)(void*)) {
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  if ((int64_t)threads > count) threads = count > 0 ? (int)count : 1;
+  pthread_t tid[256];
+  sf_chunk_t ks[256];
+  int err = 0;
+  for (int t = 0; t < threads; ++t) {
+    ks[t] = *proto;
+    ks[t].lo = count * t / threads; ks[t].hi = count * (t + 1) / threads; ks[t].err = 0;
+    if (t > 0) pthread_create(&tid[t], NULL, fn, &ks[t]);
+  }
+  fn(&ks[0]);
+  for (int t = 1; t < threads; ++t) pthread_join(tid[t], NULL);
+  for (int t = 0; t < threads; ++t) err |= ks[t].err;
+  return err ? -1 : 0;
+}
+
+int sf_oracle_fit_batch(const float* images, int W, int H, int64_t count, int P, const float* inits,
+                        const sf_oracle_config_t* c, float* out_params, float* out_alpha, float* out_beta,
+                        float* out_nchi2, uint8_t* out_status, uint8_t* out_iters, int threads) {
+  const int N = W * H;
+  if (N < 1 || N > SF_ORACLE_MAXPIX || (P != 3 && P != 4) || c->max_iterations < 1 || c->max_iterations > 255)
+    return -1;
+  sf_chunk_t k;
+  memset(&k, 0, sizeof(k));
+  k.images = images; k.W = W; k.H = H; k.P = P; k.inits = inits; k.c = c;
+  k.out_params = out_params; k.out_alpha = out_alpha; k.out_beta = out_beta; k.out_nchi2 = out_nchi2;
+  k.out_status = out_status; k.out_iters = out_iters;
+  return run_chunks(&k, count, threads, fit_chunk);
+}
+
+int sf_oracle_eval_batch(const float* images, int W, int H, int64_t count, int P, const float* params,
+                         sf_oracle_eval_t* out, int threads) {
+  sf_chunk_t k;
+  memset(&k, 0, sizeof(k));
+  k.images = images; k.W = W; k.H = H; k.P = P; k.params = params; k.eout = out;
+  return run_chunks(&k, count, threads, eval_chunk);
+}
+
+int sf_oracle_eval_size(void) { return (int)sizeof(sf_oracle_eval_t); }

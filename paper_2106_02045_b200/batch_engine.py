@@ -1,0 +1,183 @@
+"""Batch engine: fit_batch / BatchRequest over the C-ABI.
+
+Host (numpy) inputs go through ``sf_fit_batch``: contiguous shards per GPU,
+chunked H2D -> kernel -> D2H on overlapped streams, results written in index
+order.  CUDA tensors go through ``sf_fit_batch_device`` on the current torch
+stream.  Missing inits are estimated on the GPU (``sf_estimate_initial_device``,
+SPEC.md:286-290) -- the paper and SPEC time the fit without the initializer
+(PAPER.md:210), so callers that benchmark pass inits explicitly.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from .model import PixelGrid, SpotImage, params_array
+from .solver import FitConfig, FitResult, StopReason
+
+ENGINES = {"implicit3": 3, "symmetric": 3, "implicit4": 4, "elliptical": 4}
+
+
+@dataclass
+class BatchRequest:
+    """images share one grid; inits optional."""
+
+    images: object
+    inits: object = None
+    config: FitConfig = field(default_factory=FitConfig)
+    engine: str = "implicit3"
+    devices: Optional[Sequence[int]] = None
+    grid: Optional[PixelGrid] = None
+
+
+@dataclass
+class BatchResult:
+    """Structure-of-arrays result, index-aligned with the request."""
+
+    params: np.ndarray  # (count, P) f32
+    alpha: np.ndarray
+    beta: np.ndarray
+    nchi2: np.ndarray
+    status: np.ndarray  # u8: StopReason | flags
+    iterations: np.ndarray  # u8
+    stats: dict = field(default_factory=dict)
+
+    def __len__(self) -> int:
+        return len(self.alpha)
+
+    def __getitem__(self, i: int) -> FitResult:
+        return FitResult.from_row(self.params[i], self.alpha[i], self.beta[i], self.nchi2[i], self.status[i],
+                                  self.iterations[i])
+
+    @property
+    def stop(self) -> np.ndarray:
+        return (self.status & 7).astype(np.uint8)
+
+    @property
+    def no_improvement(self) -> np.ndarray:
+        return (self.status & _lib.SF_FLAG_NOIMP) != 0
+
+    def to_list(self):
+        return [self[i] for i in range(len(self))]
+
+
+def _as_image_array(images, grid: Optional[PixelGrid]):
+    """-> (array (count, N) float32 numpy or CUDA tensor, grid)."""
+    try:
+        import torch
+
+        if isinstance(images, torch.Tensor):
+            if grid is None:
+                if images.dim() != 3:
+                    raise ValueError("pass grid= for flattened image tensors")
+                grid = PixelGrid(images.shape[2], images.shape[1])
+            t = images.reshape(images.shape[0], -1)
+            if t.dtype != torch.float32:
+                t = t.float()
+            return t.contiguous(), grid
+    except ImportError:
+        pass
+    if isinstance(images, (list, tuple)) and images and isinstance(images[0], SpotImage):
+        grid = grid or images[0].grid
+        if any(im.grid != grid for im in images):
+            raise ValueError("all images in a batch must share one grid (SPEC.md:377)")
+        return np.stack([im.values for im in images]), grid
+    a = np.asarray(images, dtype=np.float32)
+    if grid is None:
+        if a.ndim != 3:
+            raise ValueError("images must be (count, H, W), a list of SpotImage, or pass grid=")
+        grid = PixelGrid(a.shape[2], a.shape[1])
+    a = np.ascontiguousarray(a.reshape(a.shape[0] if a.ndim > 1 else 1, -1))
+    if a.shape[1] != grid.n:
+        raise ValueError(f"expected {grid.n} pixel values per image, got {a.shape[1]}")
+    return a, grid
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+def fit_batch(images, inits=None, config: FitConfig = FitConfig(), engine: str = "implicit3",
+              devices: Optional[Sequence[int]] = None, grid: Optional[PixelGrid] = None,
+              out: Optional[BatchResult] = None) -> BatchResult:
+    """SPEC.md:381-389.  results[i] corresponds to images[i]; per-spot
+    failures are status bytes, never exceptions."""
+    if isinstance(images, BatchRequest):
+        r = images
+        return fit_batch(r.images, r.inits, r.config, r.engine, r.devices, r.grid, out)
+    if engine not in ENGINES:
+        if engine == "explicit5":
+            raise NotImplementedError("explicit5 (SPEC.md:229-235) is a comparison baseline outside this build")
+        raise ValueError(f"unknown engine {engine!r}")
+    P = ENGINES[engine]
+    imgs, grid = _as_image_array(images, grid)
+    count = int(imgs.shape[0])
+    L = _lib.lib()
+    _lib.require_gpu()
+    ccfg = config.to_c(grid, P)
+    is_cuda = not isinstance(imgs, np.ndarray)
+
+    if is_cuda:
+        import torch
+
+        dev = imgs.device
+        if inits is None:
+            ini = estimate_initial_device(imgs, grid, P, config)
+        else:
+            ini = torch.as_tensor(params_array(inits) if not isinstance(inits, torch.Tensor) else inits,
+                                  dtype=torch.float32, device=dev).reshape(count, P).contiguous()
+        par = torch.empty((count, P), dtype=torch.float32, device=dev)
+        fl = torch.empty((3, count), dtype=torch.float32, device=dev)
+        u8 = torch.empty((2, count), dtype=torch.uint8, device=dev)
+        ev = torch.zeros(3, dtype=torch.int64, device=dev)
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        _lib.check(L.sf_fit_batch_device(imgs.data_ptr(), grid.width, grid.height, count, ini.data_ptr(),
+                                         ctypes.byref(ccfg), par.data_ptr(), fl[0].data_ptr(), fl[1].data_ptr(),
+                                         fl[2].data_ptr(), u8[0].data_ptr(), u8[1].data_ptr(), ev.data_ptr(), stream))
+        torch.cuda.current_stream(dev).synchronize()
+        evs = ev.cpu().tolist()
+        return BatchResult(par.cpu().numpy(), fl[0].cpu().numpy(), fl[1].cpu().numpy(), fl[2].cpu().numpy(),
+                           u8[0].cpu().numpy(), u8[1].cpu().numpy(),
+                           dict(n_gradient_evals=evs[0], n_trial_evals=evs[1], n_kernel_evals=evs[2]))
+
+    if inits is None:
+        import torch
+
+        ini = estimate_initial_device(torch.as_tensor(imgs).cuda(), grid, P, config).cpu().numpy()
+    else:
+        ini = np.ascontiguousarray(params_array(inits), dtype=np.float32).reshape(count, P)
+    if out is None:
+        out = BatchResult(np.empty((count, P), np.float32), np.empty(count, np.float32), np.empty(count, np.float32),
+                          np.empty(count, np.float32), np.empty(count, np.uint8), np.empty(count, np.uint8))
+    st = _lib.sf_stats()
+    devs = list(devices) if devices else [0]
+    dev_arr = (ctypes.c_int32 * len(devs))(*devs)
+    _lib.check(L.sf_fit_batch(_ptr(imgs), grid.width, grid.height, count, _ptr(ini), ctypes.byref(ccfg),
+                              _ptr(out.params), _ptr(out.alpha), _ptr(out.beta), _ptr(out.nchi2), _ptr(out.status),
+                              _ptr(out.iterations), dev_arr, len(devs), ctypes.byref(st)))
+    out.stats = dict(n_gradient_evals=st.n_gradient_evals, n_trial_evals=st.n_trial_evals,
+                     n_kernel_evals=st.n_kernel_evals, total_ms=st.total_ms, n_devices=st.n_devices,
+                     n_chunks=st.n_chunks)
+    return out
+
+
+def estimate_initial_device(images_cuda, grid: PixelGrid, P: int, config: FitConfig = FitConfig(), amps=False):
+    """GPU initializer on a CUDA tensor (count, N) -> (count, P) [, (count, 2)]."""
+    import torch
+
+    b = config.resolved_bounds(grid)
+    count = images_cuda.shape[0]
+    ini = torch.empty((count, P), dtype=torch.float32, device=images_cuda.device)
+    am = torch.empty((count, 2), dtype=torch.float32, device=images_cuda.device) if amps else None
+    stream = torch.cuda.current_stream(images_cuda.device).cuda_stream
+    _lib.check(_lib.lib().sf_estimate_initial_device(images_cuda.data_ptr(), grid.width, grid.height, count, P,
+                                                      b.sigma_min, b.sigma_max, ini.data_ptr(),
+                                                      am.data_ptr() if am is not None else None, stream))
+    return (ini, am) if amps else ini
+
+
+__all__ = ["BatchRequest", "BatchResult", "fit_batch", "estimate_initial_device", "StopReason", "ENGINES"]

@@ -1,0 +1,540 @@
+// sf_capi.cu -- the C-ABI (include/spotfit.h): argument checking, lane
+// geometry, kernel dispatch, and the host-side batch scheduler (chunked
+// H2D -> kernel -> D2H over round-robin streams, one host thread per device,
+// contiguous shards, no collectives -- SURVEY 8e).
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "sf_geometry.h"
+#include "sf_launch.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return -1;
+}
+
+#define SF_CUDA(call)                                                                         \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess) return fail("%s failed: %s", #call, cudaGetErrorString(e_));       \
+  } while (0)
+
+int check_grid(int W, int H) {
+  if (W < 1 || H < 1) return fail("degenerate grid %dx%d", W, H);                   // model.py:53-54
+  if ((int64_t)W * H > 1024) return fail("grid %dx%d exceeds 1024 pixels", W, H);  // model.py:55-58
+  return 0;
+}
+
+int make_cfg(const sf_config* c, int W, int H, sf::Cfg& k) {
+  if (c == nullptr) return fail("cfg is NULL");
+  if (c->model != SF_MODEL_SYMMETRIC && c->model != SF_MODEL_ELLIPTICAL) return fail("model must be 3 or 4");
+  if (c->max_iterations < 1 || c->max_iterations > 255) return fail("max_iterations must be in [1, 255]");
+  if (!(c->min_delta > 0) || !(c->min_step > 0)) return fail("min_delta and min_step must be > 0");
+  if (!(c->max_error >= 0)) return fail("max_error must be >= 0");
+  if (!(c->lambda_init > 0) || !(c->lambda_init < c->lambda_max)) return fail("need 0 < lambda_init < lambda_max");
+  if (!(c->lambda_up > 0) || !(c->lambda_down > 0)) return fail("lambda factors must be > 0");
+  if (!(c->sigma_min > 0) || !(c->sigma_max > c->sigma_min)) return fail("need 0 < sigma_min < sigma_max");
+  if (!(c->margin_x >= 0) || !(c->margin_y >= 0)) return fail("margins must be >= 0");
+  k.max_it = c->max_iterations;
+  k.max_error = c->max_error;
+  k.min_delta = c->min_delta;
+  k.min_step = c->min_step;
+  k.lam0 = c->lambda_init;
+  k.lam_up = c->lambda_up;
+  k.lam_down = c->lambda_down;
+  k.lam_max = c->lambda_max;
+  k.lo[0] = -c->margin_x;
+  k.hi[0] = (double)(W - 1) + c->margin_x;
+  k.lo[1] = -c->margin_y;
+  k.hi[1] = (double)(H - 1) + c->margin_y;
+  k.lo[2] = k.lo[3] = c->sigma_min;
+  k.hi[2] = k.hi[3] = c->sigma_max;
+  return 0;
+}
+
+int sm_count_of_current() {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms > 0 ? sms : 1;
+}
+
+int dispatch_fit(int P, int slots, int ppl, const sf::LaunchFit& a) {
+  cudaError_t err = cudaSuccess;
+  int used = -1;
+#define SF_CASE(PP, S) \
+  if (P == PP && slots == S) used = sf::launch_fit_P##PP##_S##S(ppl, a, &err);
+  SF_CASE(3, 1) SF_CASE(3, 2) SF_CASE(3, 4) SF_CASE(3, 8) SF_CASE(3, 16)
+  SF_CASE(4, 1) SF_CASE(4, 2) SF_CASE(4, 4) SF_CASE(4, 8) SF_CASE(4, 16)
+#undef SF_CASE
+  if (used < 0) return fail("no kernel instantiation for P=%d slots=%d ppl=%d", P, slots, ppl);
+  if (err != cudaSuccess) return fail("fit kernel launch failed: %s", cudaGetErrorString(err));
+  return 0;
+}
+
+int dispatch_eval(int P, int slots, int ppl, const sf::LaunchEval& a) {
+  cudaError_t err = cudaSuccess;
+  int used = -1;
+#define SF_CASE(PP, S) \
+  if (P == PP && slots == S) used = sf::launch_eval_P##PP##_S##S(ppl, a, &err);
+  SF_CASE(3, 1) SF_CASE(3, 2) SF_CASE(3, 4) SF_CASE(3, 8) SF_CASE(3, 16)
+  SF_CASE(4, 1) SF_CASE(4, 2) SF_CASE(4, 4) SF_CASE(4, 8) SF_CASE(4, 16)
+#undef SF_CASE
+  if (used < 0) return fail("no kernel instantiation for P=%d slots=%d ppl=%d", P, slots, ppl);
+  if (err != cudaSuccess) return fail("eval kernel launch failed: %s", cudaGetErrorString(err));
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Per-device context: streams, device chunk buffers, pinned staging, events.
+// ---------------------------------------------------------------------------
+constexpr int kStreams = 3;
+
+struct Slot {
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[4] = {};  // start, h2d done, kernel done, d2h done
+  float* d_img = nullptr;
+  float* d_init = nullptr;
+  float* d_par = nullptr;
+  float* d_a = nullptr;
+  float* d_b = nullptr;
+  float* d_c = nullptr;
+  uint8_t* d_st = nullptr;
+  uint8_t* d_it = nullptr;
+  float* h_in = nullptr;   // pinned staging (pageable callers): images then inits
+  float* h_out = nullptr;  // pinned staging: params, alpha, beta, nchi2, status, iters
+  size_t cap_spots = 0, cap_npix = 0;
+  bool pending = false;  // staged results of a finished chunk waiting to be copied out
+  int64_t p_lo = 0, p_n = 0;
+};
+
+struct DevCtx {
+  std::mutex mu;
+  bool init = false;
+  int sms = 1;
+  Slot slot[kStreams];
+  unsigned long long* d_evals = nullptr;
+};
+
+std::mutex g_ctx_mu;
+std::vector<std::unique_ptr<DevCtx>> g_ctx;
+
+DevCtx* ctx_for(int dev) {
+  std::lock_guard<std::mutex> lk(g_ctx_mu);
+  if ((int)g_ctx.size() <= dev) g_ctx.resize(dev + 1);
+  if (!g_ctx[dev]) g_ctx[dev].reset(new DevCtx());
+  return g_ctx[dev].get();
+}
+
+void free_slot_buffers(Slot& s) {
+  cudaFree(s.d_img); cudaFree(s.d_init); cudaFree(s.d_par); cudaFree(s.d_a); cudaFree(s.d_b); cudaFree(s.d_c);
+  cudaFree(s.d_st); cudaFree(s.d_it);
+  cudaFreeHost(s.h_in); cudaFreeHost(s.h_out);
+  s.d_img = s.d_init = s.d_par = s.d_a = s.d_b = s.d_c = nullptr;
+  s.d_st = s.d_it = nullptr;
+  s.h_in = s.h_out = nullptr;
+  s.cap_spots = 0;
+}
+
+int ensure_ctx(DevCtx& c, int dev, size_t spots, int npix, int P, bool staging) {
+  if (!c.init) {
+    SF_CUDA(cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev));
+    for (auto& s : c.slot) {
+      SF_CUDA(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+      for (auto& e : s.ev) SF_CUDA(cudaEventCreate(&e));
+    }
+    SF_CUDA(cudaMalloc(&c.d_evals, 3 * sizeof(unsigned long long)));
+    c.init = true;
+  }
+  for (auto& s : c.slot) {
+    const bool grow = s.cap_spots < spots || s.cap_npix < (size_t)npix || (staging && s.h_in == nullptr);
+    if (!grow) continue;
+    free_slot_buffers(s);
+    SF_CUDA(cudaMalloc(&s.d_img, spots * npix * sizeof(float)));
+    SF_CUDA(cudaMalloc(&s.d_init, spots * 4 * sizeof(float)));
+    SF_CUDA(cudaMalloc(&s.d_par, spots * 4 * sizeof(float)));
+    SF_CUDA(cudaMalloc(&s.d_a, spots * sizeof(float)));
+    SF_CUDA(cudaMalloc(&s.d_b, spots * sizeof(float)));
+    SF_CUDA(cudaMalloc(&s.d_c, spots * sizeof(float)));
+    SF_CUDA(cudaMalloc(&s.d_st, spots));
+    SF_CUDA(cudaMalloc(&s.d_it, spots));
+    if (staging) {
+      SF_CUDA(cudaHostAlloc(&s.h_in, spots * (npix + 4) * sizeof(float), cudaHostAllocPortable));
+      SF_CUDA(cudaHostAlloc(&s.h_out, spots * (4 + 3 + 1) * sizeof(float), cudaHostAllocPortable));
+    }
+    s.cap_spots = spots;
+    s.cap_npix = npix;
+  }
+  (void)P;
+  return 0;
+}
+
+bool is_device_ptr(const void* p, int* dev) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) {
+    if (dev) *dev = a.device;
+    return true;
+  }
+  return false;
+}
+
+bool is_pinned_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+struct HostJob {
+  const float* images;
+  const float* inits;
+  int W, H, P;
+  int64_t lo, hi;
+  const sf_config* cfg;
+  float *par, *alpha, *beta, *nchi2;
+  uint8_t *status, *iters;
+  bool pinned_in, pinned_out;
+  // results
+  unsigned long long evals[3] = {0, 0, 0};
+  double h2d_ms = 0, kernel_ms = 0, d2h_ms = 0;
+  int chunks = 0;
+  int rc = 0;
+  std::string err;
+};
+
+void copy_out_staged(Slot& s, HostJob& j) {
+  if (!s.pending) return;
+  const int P = j.P;
+  const int64_t n = s.p_n, lo = s.p_lo;
+  const float* o = s.h_out;
+  const size_t cap = s.cap_spots;
+  std::memcpy(j.par + lo * P, o, n * P * sizeof(float));
+  std::memcpy(j.alpha + lo, o + cap * 4, n * sizeof(float));
+  std::memcpy(j.beta + lo, o + cap * 5, n * sizeof(float));
+  std::memcpy(j.nchi2 + lo, o + cap * 6, n * sizeof(float));
+  const uint8_t* b = reinterpret_cast<const uint8_t*>(o + cap * 7);
+  std::memcpy(j.status + lo, b, n);
+  std::memcpy(j.iters + lo, b + cap, n);
+  s.pending = false;
+}
+
+int run_shard(int dev, HostJob& j) {
+  SF_CUDA(cudaSetDevice(dev));
+  DevCtx* c = ctx_for(dev);
+  std::lock_guard<std::mutex> lk(c->mu);
+  const int N = j.W * j.H, P = j.P;
+  const int64_t total = j.hi - j.lo;
+  if (total <= 0) return 0;
+  sf::Geom geom;
+  const int ppl = sf::build_geom(j.W, j.H, P, geom);
+  sf::Cfg kc;
+  if (make_cfg(j.cfg, j.W, j.H, kc) != 0) return -1;
+  // chunking: >= 8 chunks for overlap when the shard is large, bounded buffers
+  int64_t chunk = std::max<int64_t>(16384, (total + 7) / 8);
+  chunk = std::min<int64_t>(chunk, std::max<int64_t>(16384, (int64_t)(96 << 20) / (4 * N)));
+  chunk = std::min<int64_t>(chunk, total);
+  const bool staging = !(j.pinned_in && j.pinned_out);
+  if (ensure_ctx(*c, dev, (size_t)chunk, N, P, staging) != 0) return -1;
+  SF_CUDA(cudaMemsetAsync(c->d_evals, 0, 3 * sizeof(unsigned long long), c->slot[0].stream));
+  SF_CUDA(cudaStreamSynchronize(c->slot[0].stream));
+  std::vector<int64_t> chunk_lo;
+  for (int64_t lo = 0; lo < total; lo += chunk) chunk_lo.push_back(lo);
+  for (size_t ci = 0; ci < chunk_lo.size(); ++ci) {
+    Slot& s = c->slot[ci % kStreams];
+    const int64_t lo = j.lo + chunk_lo[ci];
+    const int64_t n = std::min<int64_t>(chunk, total - chunk_lo[ci]);
+    if (staging) {  // the slot's previous chunk must be finished before its staging is reused
+      SF_CUDA(cudaEventSynchronize(s.ev[3]));
+      copy_out_staged(s, j);
+    }
+    SF_CUDA(cudaEventRecord(s.ev[0], s.stream));
+    const float* src_img = j.images + lo * N;
+    const float* src_init = j.inits + lo * P;
+    if (!j.pinned_in) {
+      std::memcpy(s.h_in, src_img, n * N * sizeof(float));
+      std::memcpy(s.h_in + s.cap_spots * N, src_init, n * P * sizeof(float));
+      src_img = s.h_in;
+      src_init = s.h_in + s.cap_spots * N;
+    }
+    SF_CUDA(cudaMemcpyAsync(s.d_img, src_img, n * N * sizeof(float), cudaMemcpyHostToDevice, s.stream));
+    SF_CUDA(cudaMemcpyAsync(s.d_init, src_init, n * P * sizeof(float), cudaMemcpyHostToDevice, s.stream));
+    SF_CUDA(cudaEventRecord(s.ev[1], s.stream));
+    sf::LaunchFit a;
+    a.images = s.d_img;
+    a.inits = s.d_init;
+    a.count = n;
+    a.geom = geom;
+    a.cfg = kc;
+    a.out = sf::FitOut{s.d_par, s.d_a, s.d_b, s.d_c, s.d_st, s.d_it, c->d_evals};
+    a.stream = s.stream;
+    a.sm_count = c->sms;
+    if (dispatch_fit(P, geom.slots, ppl, a) != 0) return -1;
+    SF_CUDA(cudaEventRecord(s.ev[2], s.stream));
+    if (j.pinned_out) {
+      SF_CUDA(cudaMemcpyAsync(j.par + lo * P, s.d_par, n * P * sizeof(float), cudaMemcpyDeviceToHost, s.stream));
+      SF_CUDA(cudaMemcpyAsync(j.alpha + lo, s.d_a, n * sizeof(float), cudaMemcpyDeviceToHost, s.stream));
+      SF_CUDA(cudaMemcpyAsync(j.beta + lo, s.d_b, n * sizeof(float), cudaMemcpyDeviceToHost, s.stream));
+      SF_CUDA(cudaMemcpyAsync(j.nchi2 + lo, s.d_c, n * sizeof(float), cudaMemcpyDeviceToHost, s.stream));
+      SF_CUDA(cudaMemcpyAsync(j.status + lo, s.d_st, n, cudaMemcpyDeviceToHost, s.stream));
+      SF_CUDA(cudaMemcpyAsync(j.iters + lo, s.d_it, n, cudaMemcpyDeviceToHost, s.stream));
+    } else {
+      float* o = s.h_out;
+      const size_t cap = s.cap_spots;
+      uint8_t* b = reinterpret_cast<uint8_t*>(o + cap * 7);
+      SF_CUDA(cudaMemcpyAsync(o, s.d_par, n * P * sizeof(float), cudaMemcpyDeviceToHost, s.stream));
+      SF_CUDA(cudaMemcpyAsync(o + cap * 4, s.d_a, n * sizeof(float), cudaMemcpyDeviceToHost, s.stream));
+      SF_CUDA(cudaMemcpyAsync(o + cap * 5, s.d_b, n * sizeof(float), cudaMemcpyDeviceToHost, s.stream));
+      SF_CUDA(cudaMemcpyAsync(o + cap * 6, s.d_c, n * sizeof(float), cudaMemcpyDeviceToHost, s.stream));
+      SF_CUDA(cudaMemcpyAsync(b, s.d_st, n, cudaMemcpyDeviceToHost, s.stream));
+      SF_CUDA(cudaMemcpyAsync(b + cap, s.d_it, n, cudaMemcpyDeviceToHost, s.stream));
+      s.pending = true;
+      s.p_lo = lo;
+      s.p_n = n;
+    }
+    SF_CUDA(cudaEventRecord(s.ev[3], s.stream));
+    ++j.chunks;
+    // per-chunk device times (informational; chunks overlap across streams)
+    if (ci + 1 >= (size_t)kStreams) {
+      Slot& old = c->slot[(ci + 1) % kStreams];
+      (void)old;
+    }
+  }
+  for (auto& s : c->slot) {
+    SF_CUDA(cudaStreamSynchronize(s.stream));
+    if (staging) copy_out_staged(s, j);
+  }
+  SF_CUDA(cudaMemcpy(j.evals, c->d_evals, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sf_version(void) { return SF_ABI_VERSION; }
+
+int sf_lane_geometry(int32_t width, int32_t height, int32_t* slots, int32_t* ppl, int16_t* nc, int16_t* nt,
+                     int16_t* base, int16_t* tbase) {
+  if (check_grid(width, height) != 0) return -1;
+  sf::Geom g;
+  const int need = sf::build_geom(width, height, 3, g);
+  if (slots) *slots = g.slots;
+  if (ppl) *ppl = need;
+  for (int l = 0; l < g.lanes; ++l) {
+    if (nc) nc[l] = g.nc[l];
+    if (nt) nt[l] = g.nt[l];
+    if (base) base[l] = g.base[l];
+    if (tbase) tbase[l] = g.tbase[l];
+  }
+  return 0;
+}
+
+const char* sf_last_error(void) { return g_err.c_str(); }
+
+int sf_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+void* sf_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    fail("cudaHostAlloc(%zu) failed", bytes);
+    return nullptr;
+  }
+  return p;
+}
+
+void sf_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+int sf_fit_batch_device(const float* d_images, int32_t width, int32_t height, int64_t count, const float* d_inits,
+                        const sf_config* cfg, float* d_params, float* d_alpha, float* d_beta, float* d_nchi2,
+                        uint8_t* d_status, uint8_t* d_iters, uint64_t* d_evals, void* stream) {
+  if (check_grid(width, height) != 0) return -1;
+  if (count < 0) return fail("negative count");
+  sf::Cfg kc;
+  if (make_cfg(cfg, width, height, kc) != 0) return -1;
+  if (count == 0) return 0;
+  if (!d_images || !d_inits || !d_params || !d_alpha || !d_beta || !d_nchi2 || !d_status || !d_iters)
+    return fail("NULL buffer");
+  sf::Geom geom;
+  const int ppl = sf::build_geom(width, height, cfg->model, geom);
+  sf::LaunchFit a;
+  a.images = d_images;
+  a.inits = d_inits;
+  a.count = count;
+  a.geom = geom;
+  a.cfg = kc;
+  a.out = sf::FitOut{d_params, d_alpha, d_beta, d_nchi2, d_status, d_iters,
+                     reinterpret_cast<unsigned long long*>(d_evals)};
+  a.stream = static_cast<cudaStream_t>(stream);
+  a.sm_count = sm_count_of_current();
+  return dispatch_fit(cfg->model, geom.slots, ppl, a);
+}
+
+int sf_eval_batch_device(const float* d_images, int32_t width, int32_t height, int64_t count, int32_t model,
+                         const float* d_params, sf_eval_record* d_out, void* stream) {
+  if (check_grid(width, height) != 0) return -1;
+  if (model != 3 && model != 4) return fail("model must be 3 or 4");
+  if (count < 0) return fail("negative count");
+  if (count == 0) return 0;
+  sf::Geom geom;
+  const int ppl = sf::build_geom(width, height, model, geom);
+  sf::LaunchEval a;
+  a.images = d_images;
+  a.params = d_params;
+  a.count = count;
+  a.geom = geom;
+  a.out = d_out;
+  a.stream = static_cast<cudaStream_t>(stream);
+  return dispatch_eval(model, geom.slots, ppl, a);
+}
+
+int sf_estimate_initial_device(const float* d_images, int32_t width, int32_t height, int64_t count, int32_t model,
+                               double sigma_min, double sigma_max, float* d_inits, float* d_amps, void* stream) {
+  if (check_grid(width, height) != 0) return -1;
+  if (model != 3 && model != 4) return fail("model must be 3 or 4");
+  if (count < 0) return fail("negative count");
+  if (!(sigma_min > 0) || !(sigma_max > sigma_min)) return fail("need 0 < sigma_min < sigma_max");
+  cudaError_t e = sf::launch_estimate_initial(d_images, width, height, count, model, sigma_min, sigma_max, d_inits,
+                                              d_amps, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail("initializer launch failed: %s", cudaGetErrorString(e));
+  return 0;
+}
+
+int sf_fit_batch(const float* images, int32_t width, int32_t height, int64_t count, const float* inits,
+                 const sf_config* cfg, float* out_params, float* out_alpha, float* out_beta, float* out_nchi2,
+                 uint8_t* out_status, uint8_t* out_iters, const int32_t* devices, int32_t n_devices,
+                 sf_stats* stats) {
+  const auto t0 = std::chrono::steady_clock::now();
+  if (check_grid(width, height) != 0) return -1;
+  if (count < 0) return fail("negative count");
+  sf::Cfg kc;
+  if (make_cfg(cfg, width, height, kc) != 0) return -1;
+  if (stats) std::memset(stats, 0, sizeof(*stats));
+  if (count == 0) return 0;
+  if (!images || !inits || !out_params || !out_alpha || !out_beta || !out_nchi2 || !out_status || !out_iters)
+    return fail("NULL buffer");
+  int ndev_avail = sf_device_count();
+  if (ndev_avail < 1) return fail("no CUDA device available (the CUDA engine has no CPU fallback)");
+  std::vector<int> devs;
+  if (devices && n_devices > 0) {
+    for (int i = 0; i < n_devices; ++i) {
+      if (devices[i] < 0 || devices[i] >= ndev_avail) return fail("device %d out of range", devices[i]);
+      devs.push_back(devices[i]);
+    }
+  } else {
+    devs.push_back(0);
+  }
+  int dptr_dev = -1;
+  if (is_device_ptr(images, &dptr_dev)) {
+    // device-resident batch: one device, synchronous call on the library stream
+    if (devs.size() > 1) return fail("device-pointer batches run on the owning device only");
+    SF_CUDA(cudaSetDevice(dptr_dev));
+    DevCtx* c = ctx_for(dptr_dev);
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (ensure_ctx(*c, dptr_dev, 1, width * height, cfg->model, false) != 0) return -1;
+    cudaStream_t st = c->slot[0].stream;
+    SF_CUDA(cudaMemsetAsync(c->d_evals, 0, 3 * sizeof(unsigned long long), st));
+    SF_CUDA(cudaEventRecord(c->slot[0].ev[1], st));
+    if (sf_fit_batch_device(images, width, height, count, inits, cfg, out_params, out_alpha, out_beta, out_nchi2,
+                            out_status, out_iters, reinterpret_cast<uint64_t*>(c->d_evals), st) != 0)
+      return -1;
+    SF_CUDA(cudaEventRecord(c->slot[0].ev[2], st));
+    SF_CUDA(cudaStreamSynchronize(st));
+    if (stats) {
+      unsigned long long ev[3];
+      SF_CUDA(cudaMemcpy(ev, c->d_evals, sizeof(ev), cudaMemcpyDeviceToHost));
+      float ms = 0;
+      cudaEventElapsedTime(&ms, c->slot[0].ev[1], c->slot[0].ev[2]);
+      stats->n_gradient_evals = ev[0];
+      stats->n_trial_evals = ev[1];
+      stats->n_kernel_evals = ev[2];
+      stats->kernel_ms = ms;
+      stats->n_devices = 1;
+      stats->n_chunks = 1;
+      stats->total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+    return 0;
+  }
+  const bool pin_in = is_pinned_ptr(images) && is_pinned_ptr(inits);
+  const bool pin_out = is_pinned_ptr(out_params) && is_pinned_ptr(out_alpha) && is_pinned_ptr(out_beta) &&
+                       is_pinned_ptr(out_nchi2) && is_pinned_ptr(out_status) && is_pinned_ptr(out_iters);
+  const int nd = (int)devs.size();
+  std::vector<HostJob> jobs(nd);
+  for (int d = 0; d < nd; ++d) {
+    HostJob& j = jobs[d];
+    j.images = images;
+    j.inits = inits;
+    j.W = width;
+    j.H = height;
+    j.P = cfg->model;
+    j.lo = count * d / nd;
+    j.hi = count * (d + 1) / nd;
+    j.cfg = cfg;
+    j.par = out_params;
+    j.alpha = out_alpha;
+    j.beta = out_beta;
+    j.nchi2 = out_nchi2;
+    j.status = out_status;
+    j.iters = out_iters;
+    j.pinned_in = pin_in;
+    j.pinned_out = pin_out;
+  }
+  std::vector<std::thread> th;
+  for (int d = 1; d < nd; ++d)
+    th.emplace_back([&, d]() {
+      jobs[d].rc = run_shard(devs[d], jobs[d]);
+      if (jobs[d].rc != 0) jobs[d].err = g_err;
+    });
+  jobs[0].rc = run_shard(devs[0], jobs[0]);
+  if (jobs[0].rc != 0) jobs[0].err = g_err;
+  for (auto& t : th) t.join();
+  for (int d = 0; d < nd; ++d)
+    if (jobs[d].rc != 0) return fail("device %d: %s", devs[d], jobs[d].err.c_str());
+  if (stats) {
+    for (auto& j : jobs) {
+      stats->n_gradient_evals += j.evals[0];
+      stats->n_trial_evals += j.evals[1];
+      stats->n_kernel_evals += j.evals[2];
+      stats->n_chunks += j.chunks;
+    }
+    stats->n_devices = nd;
+    stats->total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,335 @@
+// sf_fit_kernel.cuh -- the fused, device-resident LM fit kernel (sm_100a).
+//
+// One "group" of 8*SLOTS chain lanes fits one spot at a time; groups are
+// persistent and walk the batch with a static stride (spot = gid, gid+G, ...),
+// so a group that stops early simply loads its next spot while its warp-mates
+// keep iterating.  Each loop trip is: [refill groups that finished] ->
+// one fused evaluation (sf_device.cuh:evaluate) -> the LM state machine of
+// SURVEY App. A, which is divergent across groups but
+// cheap.  No host round trip happens inside a fit.
+#pragma once
+#include "sf_device.cuh"
+
+namespace sf {
+
+struct FitOut {
+  float* params;
+  float* alpha;
+  float* beta;
+  float* nchi2;
+  uint8_t* status;
+  uint8_t* iters;
+  unsigned long long* evals;  // [3]: reference G-evals, reference T-evals, fused kernel evals (or null)
+};
+
+// Per-spot LM state, replicated in every lane of the group.
+template <int P>
+struct LMState {
+  float p[P];     // parameters under evaluation (G point or trial point)
+  float best[P];  // PAPER.md:144 "best := current"
+  double delta[P];
+  double lam;
+  double jtj[P * (P + 1) / 2], rhs[P];  // normal system at best
+  float chib, ab, bb;                   // chi^2, alpha, beta at best
+  int it;
+  bool trial, first, small;
+};
+
+template <int P>
+__device__ __forceinline__ void write_result(const FitOut& o, int64_t spot, bool leader, const float (&p)[P],
+                                             bool singular, float chi, float a, float b, int n_pix, int status,
+                                             int it) {
+  if (!leader) return;
+#pragma unroll
+  for (int k = 0; k < P; ++k) o.params[spot * P + k] = p[k];
+  if (singular) {
+    o.alpha[spot] = __int_as_float(0x7fc00000);
+    o.beta[spot] = __int_as_float(0x7fc00000);
+    o.nchi2[spot] = __int_as_float(0x7fc00000);
+  } else {
+    o.alpha[spot] = a;
+    o.beta[spot] = b;
+    // normalized_chi: chi^2/(N-5) in f64, quantised to f32
+    o.nchi2[spot] = n_pix > 5 ? (float)((double)chi / (double)(n_pix - 5)) : chi;
+  }
+  o.status[spot] = (uint8_t)status;
+  o.iters[spot] = (uint8_t)it;
+}
+
+// Consume one evaluation; returns true when the spot's fit has finished (result written).
+// Mirrors oracle/lm.py:fit_single line for line (App. A), with the accepted
+// trial's evaluation reused as the next iteration's G-eval ([A6]).
+template <int P>
+__device__ __forceinline__ bool lm_step(LMState<P>& s, const Eval<P>& E, const Cfg& c, const FitOut& o,
+                                        int64_t spot, bool leader, int n_pix, unsigned& n_g, unsigned& n_t) {
+  constexpr int T = P * (P + 1) / 2;
+  float chit = 0.0f;
+  bool small = s.small;
+  int action;  // 0: process E as G-eval, 1: solve a trial, 2: post-trial decision
+  if (s.trial) {
+    chit = E.singular ? __int_as_float(0x7fc00000) : E.chi;
+    action = 2;
+  } else {
+    action = 0;
+  }
+#pragma unroll 1
+  for (;;) {
+    if (action == 0) {
+      s.it += 1;
+      n_g += 1;
+      if (E.singular || !isfinite(E.chi)) {
+        write_result<P>(o, spot, leader, s.p, E.singular, E.chi, E.alpha, E.beta, n_pix, SF_STOP_NOT_CONVERGED, s.it);
+        return true;
+      }
+      if ((double)E.chi < c.max_error) {
+        write_result<P>(o, spot, leader, s.p, false, E.chi, E.alpha, E.beta, n_pix, SF_STOP_MAX_ERROR, s.it);
+        return true;
+      }
+      s.chib = E.chi;
+      s.ab = E.alpha;
+      s.bb = E.beta;
+#pragma unroll
+      for (int k = 0; k < P; ++k) { s.best[k] = s.p[k]; s.rhs[k] = E.rhs[k]; }
+#pragma unroll
+      for (int m = 0; m < T; ++m) s.jtj[m] = E.jtj[m];
+      s.first = true;
+      action = 1;
+    }
+    if (action == 1) {  // PAPER.md:147-151 (and the retry body 159-164)
+      if (solve_step<P>(s.jtj, s.rhs, s.lam, s.delta)) {
+        double v[P];
+        small = true;
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+          v[k] = (double)s.best[k] + s.delta[k];
+          const double thr = c.min_step * fmax(fabs((double)s.best[k]), 1.0);
+          small = small && (fabs(s.delta[k]) < thr);
+        }
+        limit_params<P>(c, v, s.p);
+        s.small = small;
+        s.trial = true;
+        n_t += 1;
+        return false;  // evaluate the trial point next
+      }
+      chit = __int_as_float(0x7f800000);  // StepFailed: chi'^2 = +inf, not small
+      small = false;
+      action = 2;
+    }
+    // action == 2: PAPER.md:153-174
+    if (s.first) {
+      s.first = false;
+      if (s.chib > chit) s.lam = s.lam / c.lam_down;
+    }
+    if (!small && s.chib < chit && s.lam < c.lam_max) {
+      s.lam = s.lam * c.lam_up;
+      action = 1;
+      continue;
+    }
+    if (isnan(chit) || (s.chib < chit && s.lam >= c.lam_max)) {
+      write_result<P>(o, spot, leader, s.best, false, s.chib, s.ab, s.bb, n_pix, SF_STOP_NOT_CONVERGED, s.it);
+      return true;
+    }
+    if (s.chib < chit) {
+      write_result<P>(o, spot, leader, s.best, false, s.chib, s.ab, s.bb, n_pix, SF_STOP_MIN_DELTA | SF_FLAG_NOIMP,
+                      s.it);
+      return true;
+    }
+    if ((double)chit < c.max_error) {
+      write_result<P>(o, spot, leader, s.p, false, E.chi, E.alpha, E.beta, n_pix, SF_STOP_MAX_ERROR, s.it);
+      return true;
+    }
+    if ((double)s.chib * (1.0 - c.min_delta) < (double)chit) {
+      write_result<P>(o, spot, leader, s.p, false, E.chi, E.alpha, E.beta, n_pix, SF_STOP_MIN_DELTA, s.it);
+      return true;
+    }
+    if (small) {
+      write_result<P>(o, spot, leader, s.p, false, E.chi, E.alpha, E.beta, n_pix, SF_STOP_MIN_STEP, s.it);
+      return true;
+    }
+    if (s.it >= c.max_it) {
+      write_result<P>(o, spot, leader, s.p, false, E.chi, E.alpha, E.beta, n_pix, SF_STOP_MAX_ITERATIONS, s.it);
+      return true;
+    }
+    // accepted, budget left: E is exactly the next iteration's G-eval at s.p
+    s.trial = false;
+    action = 0;
+  }
+}
+
+template <int SLOTS>
+constexpr int threads_per_block() {
+  return SLOTS >= 8 ? 8 * SLOTS : 128;
+}
+
+template <int P, int PPL, int SLOTS>
+__global__ void __launch_bounds__(threads_per_block<SLOTS>())
+    fit_kernel(const float* __restrict__ images, const float* __restrict__ inits, int64_t count, const Geom geom,
+               const Cfg cfg, FitOut out) {
+  constexpr int LANES = 8 * SLOTS;
+  __shared__ double sm[kSmemDoubles<SLOTS>];
+  const int lane = threadIdx.x & 31;
+  int gl;
+  int64_t gid, ngroups;
+  if constexpr (SLOTS >= 8) {
+    gl = threadIdx.x;
+    gid = blockIdx.x;
+    ngroups = gridDim.x;
+  } else {
+    constexpr int GPW = 32 / LANES;
+    gl = lane % LANES;
+    gid = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * GPW + lane / LANES;
+    ngroups = (int64_t)gridDim.x * (blockDim.x >> 5) * GPW;
+  }
+  const bool leader = gl == 0;
+  const int N = geom.N;
+  const int nc = geom.nc[gl], nt = geom.nt[gl];
+  const int base = geom.base[gl], tbase = geom.tbase[gl];
+  const double n = (double)N;
+
+  // lane-constant pixel coordinates (model.py:35-41)
+  float xs[PPL], ys[PPL];
+  int off[PPL];
+#pragma unroll
+  for (int j = 0; j < PPL; ++j) {
+    int pix = j < nc ? base + 8 * j : (j < nc + nt ? tbase + (j - nc) : -1);
+    off[j] = pix;
+    const int pp = pix < 0 ? 0 : pix;
+    xs[j] = (float)(pp % geom.W);
+    ys[j] = (float)(pp / geom.W);
+  }
+
+  float g[PPL];
+  double G = 0.0;
+  LMState<P> s;
+  int64_t spot = gid - ngroups;
+  bool need = true, exhausted = false;
+  unsigned n_g = 0, n_t = 0, n_e = 0;
+
+#pragma unroll 1
+  for (;;) {
+    if (__any_sync(kFull, need)) {
+      // ---- refill: next spot for every group whose fit finished
+      if (need) {
+        spot += ngroups;
+        exhausted = spot >= count;
+      }
+      const bool load = need && !exhausted;
+      bool bad = false;
+      if (load) {
+        const float* img = images + spot * (int64_t)N;
+#pragma unroll
+        for (int j = 0; j < PPL; ++j) {
+          g[j] = off[j] >= 0 ? __ldg(img + off[j]) : 0.0f;
+          bad = bad || !isfinite(g[j]);
+        }
+        float init[P];
+        double v[P];
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+          init[k] = __ldg(inits + spot * P + k);
+          bad = bad || !isfinite(init[k]);
+          v[k] = (double)init[k];
+        }
+        limit_params<P>(cfg, v, s.p);  // SPEC.md:211 "sigma within bounds after limit"
+        s.lam = cfg.lam0;
+        s.it = 0;
+        s.trial = false;
+        s.first = false;
+        s.small = false;
+        if (bad) {  // keep the raw init for the InvalidInput result (oracle/lm.py:fit_single)
+#pragma unroll
+          for (int k = 0; k < P; ++k) s.p[k] = init[k];
+        }
+      }
+      const bool gbad = group_any<SLOTS>(bad);
+      const double gsum = pixel_sum<PPL, SLOTS>(g, nc, nt, sm);
+      if (load) {
+        G = gsum;
+        if (gbad) {
+          write_result<P>(out, spot, leader, s.p, true, 0.f, 0.f, 0.f, N, SF_STOP_NOT_CONVERGED | SF_FLAG_INVALID, 0);
+          need = true;  // fetch the next spot on the next trip
+        } else {
+          need = false;
+        }
+      } else if (need) {
+        need = false;  // exhausted
+      }
+      if (load && gbad) continue;
+    }
+    if (__all_sync(kFull, exhausted)) break;
+
+    Eval<P> E;
+    evaluate<P, PPL, SLOTS>(xs, ys, g, nc, nt, G, n, s.p, E, sm);
+    if (!exhausted) {
+      n_e += 1;
+      if (lm_step<P>(s, E, cfg, out, spot, leader, N, n_g, n_t)) need = true;
+    }
+  }
+  if (out.evals != nullptr && leader) {
+    atomicAdd(out.evals + 0, (unsigned long long)n_g);
+    atomicAdd(out.evals + 1, (unsigned long long)n_t);
+    atomicAdd(out.evals + 2, (unsigned long long)n_e);
+  }
+}
+
+// Model-level evaluation (sf_eval_batch_device): one group per spot, no LM.
+template <int P, int PPL, int SLOTS>
+__global__ void __launch_bounds__(threads_per_block<SLOTS>())
+    eval_kernel(const float* __restrict__ images, const float* __restrict__ params, int64_t count, const Geom geom,
+                sf_eval_record* __restrict__ out) {
+  constexpr int LANES = 8 * SLOTS;
+  __shared__ double sm[kSmemDoubles<SLOTS>];
+  const int lane = threadIdx.x & 31;
+  int gl;
+  int64_t gid;
+  if constexpr (SLOTS >= 8) {
+    gl = threadIdx.x;
+    gid = blockIdx.x;
+  } else {
+    constexpr int GPW = 32 / LANES;
+    gl = lane % LANES;
+    gid = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * GPW + lane / LANES;
+  }
+  const int N = geom.N;
+  const int nc = geom.nc[gl], nt = geom.nt[gl];
+  const int base = geom.base[gl], tbase = geom.tbase[gl];
+  const bool valid = gid < count;
+  const int64_t spot = valid ? gid : 0;
+  float xs[PPL], ys[PPL], g[PPL];
+  const float* img = images + spot * (int64_t)N;
+#pragma unroll
+  for (int j = 0; j < PPL; ++j) {
+    const int pix = j < nc ? base + 8 * j : (j < nc + nt ? tbase + (j - nc) : -1);
+    const int pp = pix < 0 ? 0 : pix;
+    xs[j] = (float)(pp % geom.W);
+    ys[j] = (float)(pp / geom.W);
+    g[j] = (pix >= 0 && valid) ? __ldg(img + pix) : 0.0f;
+  }
+  float pe[P];
+#pragma unroll
+  for (int k = 0; k < P; ++k) pe[k] = valid ? __ldg(params + spot * P + k) : 1.0f;
+  const double G = pixel_sum<PPL, SLOTS>(g, nc, nt, sm);
+  Eval<P> E;
+  EvalExtras<P> X;
+  evaluate<P, PPL, SLOTS, true>(xs, ys, g, nc, nt, G, (double)N, pe, E, sm, &X);
+  if (valid && gl == 0) {
+    sf_eval_record r;
+    r.singular = E.singular ? 1 : 0;
+    r.alpha = E.alpha; r.beta = E.beta; r.chi = E.chi;
+    r.F = X.F; r.G = G; r.FF = X.FF; r.FG = X.FG; r.denom = X.denom;
+    for (int k = 0; k < 4; ++k) {
+      const bool in = k < P;
+      r.dF[k] = in ? X.dF[k < P ? k : 0] : 0.0;
+      r.dFF[k] = in ? X.dFF[k < P ? k : 0] : 0.0;
+      r.dFG[k] = in ? X.dFG[k < P ? k : 0] : 0.0;
+      r.gamma[k] = in ? X.gamma[k < P ? k : 0] : 0.0;
+      r.dalpha[k] = in ? X.dalpha[k < P ? k : 0] : 0.0;
+      r.dbeta[k] = in ? X.dbeta[k < P ? k : 0] : 0.0;
+      r.rhs[k] = in ? E.rhs[k < P ? k : 0] : 0.0;
+    }
+    for (int m = 0; m < 10; ++m) r.jtj[m] = m < P * (P + 1) / 2 ? E.jtj[m < P * (P + 1) / 2 ? m : 0] : 0.0;
+    out[spot] = r;
+  }
+}
+
+}  // namespace sf

@@ -1,0 +1,88 @@
+// sf_init.cu -- GPU initializer: estimate_initial for a whole batch
+// (SURVEY 8f item 1).  One warp per spot.
+//
+// Pinned arithmetic (oracle/initializer.py restates it):
+//   smoothed_i = f32( sum_f64(in-bounds 3x3 neighbours, row-major order) / count )
+//   (x, y)     = coordinates of the first maximum of smoothed (row-major ties)
+//   beta       = min smoothed;  alpha = f32(f64(max) - f64(beta))
+//   M          = #{ i : f64(g_i) > f64(alpha) * exp(-0.5) + f64(beta) }  (original pixels)
+//   sigma      = f32( clamp( sqrt(M / pi), sigma_min, sigma_max ) )
+#include <cfloat>
+#include <climits>
+
+#include "sf_launch.h"
+
+namespace sf {
+
+namespace {
+constexpr double kExpMinusHalf = 0x1.368b2fc6f960ap-1;  // exp(-0.5), correctly rounded
+constexpr double kPi = 3.141592653589793115997963468544185161590576171875;
+
+__global__ void __launch_bounds__(256) init_kernel(const float* __restrict__ images, int W, int H, int64_t count,
+                                                   int P, double smin, double smax, float* __restrict__ inits,
+                                                   float* __restrict__ amps) {
+  const int64_t spot = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (spot >= count) return;
+  const int N = W * H;
+  const float* g = images + spot * (int64_t)N;
+  float best = -INFINITY, lo = INFINITY;
+  int bidx = INT_MAX;
+  for (int i = lane; i < N; i += 32) {
+    const int x = i % W, y = i / W;
+    double s = 0.0;
+    int cnt = 0;
+    for (int dy = -1; dy <= 1; ++dy) {
+      const int yy = y + dy;
+      if (yy < 0 || yy >= H) continue;
+      for (int dx = -1; dx <= 1; ++dx) {
+        const int xx = x + dx;
+        if (xx < 0 || xx >= W) continue;
+        s = s + (double)__ldg(g + yy * W + xx);
+        ++cnt;
+      }
+    }
+    const float v = (float)(s / (double)cnt);
+    if (v > best || (v == best && i < bidx)) { best = v; bidx = i; }
+    lo = fminf(lo, v);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+    if (ob > best || (ob == best && oi < bidx)) { best = ob; bidx = oi; }
+    lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+  }
+  if (bidx == INT_MAX) bidx = 0;
+  const float alpha = (float)((double)best - (double)lo);
+  const double thr = (double)alpha * kExpMinusHalf + (double)lo;
+  int m = 0;
+  for (int i = lane; i < N; i += 32) m += ((double)__ldg(g + i) > thr) ? 1 : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
+  double sg = sqrt((double)m / kPi);
+  sg = sg < smin ? smin : (sg > smax ? smax : sg);
+  if (lane == 0) {
+    float* o = inits + spot * P;
+    o[0] = (float)(bidx % W);
+    o[1] = (float)(bidx / W);
+    o[2] = (float)sg;
+    if (P == 4) o[3] = (float)sg;
+    if (amps != nullptr) {
+      amps[2 * spot] = alpha;
+      amps[2 * spot + 1] = lo;
+    }
+  }
+}
+}  // namespace
+
+cudaError_t launch_estimate_initial(const float* images, int W, int H, int64_t count, int P, double sigma_min,
+                                    double sigma_max, float* inits, float* amps, cudaStream_t stream) {
+  if (count <= 0) return cudaSuccess;
+  const int64_t threads = count * 32;
+  const int64_t blocks = (threads + 255) / 256;
+  init_kernel<<<(unsigned)blocks, 256, 0, stream>>>(images, W, H, count, P, sigma_min, sigma_max, inits, amps);
+  return cudaGetLastError();
+}
+
+}  // namespace sf

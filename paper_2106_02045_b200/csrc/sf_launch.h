@@ -1,0 +1,52 @@
+// sf_launch.h -- internal (C++) interface between the C-ABI layer and the
+// template instantiation units (sf_inst.cu compiled once per (P, SLOTS)).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "sf_fit_kernel.cuh"
+
+namespace sf {
+
+struct LaunchFit {
+  const float* images;
+  const float* inits;
+  int64_t count;
+  Geom geom;
+  Cfg cfg;
+  FitOut out;
+  cudaStream_t stream;
+  int sm_count;
+};
+
+struct LaunchEval {
+  const float* images;
+  const float* params;
+  int64_t count;
+  Geom geom;
+  sf_eval_record* out;
+  cudaStream_t stream;
+};
+
+// Each returns the PPL instantiation used (>= ppl_needed), or -1 if none fits;
+// a CUDA launch error is reported through *err.
+#define SF_DECLARE_UNIT(P, S)                                                      \
+  int launch_fit_P##P##_S##S(int ppl_needed, const LaunchFit& a, cudaError_t* err); \
+  int launch_eval_P##P##_S##S(int ppl_needed, const LaunchEval& a, cudaError_t* err);
+SF_DECLARE_UNIT(3, 1)
+SF_DECLARE_UNIT(3, 2)
+SF_DECLARE_UNIT(3, 4)
+SF_DECLARE_UNIT(3, 8)
+SF_DECLARE_UNIT(3, 16)
+SF_DECLARE_UNIT(4, 1)
+SF_DECLARE_UNIT(4, 2)
+SF_DECLARE_UNIT(4, 4)
+SF_DECLARE_UNIT(4, 8)
+SF_DECLARE_UNIT(4, 16)
+#undef SF_DECLARE_UNIT
+
+// initializer kernel launcher (sf_init.cu)
+cudaError_t launch_estimate_initial(const float* images, int W, int H, int64_t count, int P, double sigma_min,
+                                    double sigma_max, float* inits, float* amps, cudaStream_t stream);
+
+}  // namespace sf
