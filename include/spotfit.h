@@ -163,6 +163,13 @@ void sf_host_free(void* p);
 int sf_lane_geometry(int32_t width, int32_t height, int32_t* slots, int32_t* ppl, int16_t* nc, int16_t* nt,
                      int16_t* base, int16_t* tbase);
 
+/*
+ * sf_debug_npexp_device -- diagnostic: the kernel's float32 exp (numpy's
+ * simd_exp_f32 restated; model.py:177,193 call np.exp) on a device array.
+ * variant 0: production (fast-path IEEE division); 1: CUDA __fdiv_rn.
+ */
+int sf_debug_npexp_device(const float* d_x, float* d_y, int64_t n, int32_t variant, void* stream);
+
 int sf_device_count(void);
 const char* sf_last_error(void);
 int sf_version(void);

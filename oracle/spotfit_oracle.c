@@ -75,8 +75,29 @@ float npexp_f32(float x) {
   return ldexp_single_round(r, (int)q);
 }
 
+typedef struct { const float* x; float* y; int64_t n; } npexp_job_t;
+
+static void* npexp_job(void* a) {
+  npexp_job_t* j = (npexp_job_t*)a;
+  for (int64_t i = 0; i < j->n; ++i) j->y[i] = npexp_f32(j->x[i]);
+  return NULL;
+}
+
 void npexp_f32_array(const float* x, float* y, int64_t n) {
-  for (int64_t i = 0; i < n; ++i) y[i] = npexp_f32(x[i]);
+  enum { T = 16 };
+  if (n < (1 << 20)) {
+    npexp_job_t j = {x, y, n};
+    npexp_job(&j);
+    return;
+  }
+  pthread_t tid[T];
+  npexp_job_t jobs[T];
+  for (int t = 0; t < T; ++t) {
+    const int64_t lo = n * t / T, hi = n * (t + 1) / T;
+    jobs[t].x = x + lo; jobs[t].y = y + lo; jobs[t].n = hi - lo;
+    pthread_create(&tid[t], NULL, npexp_job, &jobs[t]);
+  }
+  for (int t = 0; t < T; ++t) pthread_join(tid[t], NULL);
 }
 
 /* ------------------------------------------------------------------ */

@@ -91,10 +91,11 @@ def _as_image_array(images, grid: Optional[PixelGrid]):
         if a.ndim != 3:
             raise ValueError("images must be (count, H, W), a list of SpotImage, or pass grid=")
         grid = PixelGrid(a.shape[2], a.shape[1])
-    a = np.ascontiguousarray(a.reshape(a.shape[0] if a.ndim > 1 else 1, -1))
-    if a.shape[1] != grid.n:
-        raise ValueError(f"expected {grid.n} pixel values per image, got {a.shape[1]}")
-    return a, grid
+    count = a.shape[0] if a.ndim > 1 else 1
+    per = a.size // count if count else (int(np.prod(a.shape[1:])) if a.ndim > 1 else 0)
+    if per != grid.n:
+        raise ValueError(f"expected {grid.n} pixel values per image, got {per}")
+    return np.ascontiguousarray(a.reshape(count, grid.n)), grid
 
 
 def _ptr(a: np.ndarray) -> int:

@@ -51,7 +51,8 @@ int make_cfg(const sf_config* c, int W, int H, sf::Cfg& k) {
   if (!(c->min_delta > 0) || !(c->min_step > 0)) return fail("min_delta and min_step must be > 0");
   if (!(c->max_error >= 0)) return fail("max_error must be >= 0");
   if (!(c->lambda_init > 0) || !(c->lambda_init < c->lambda_max)) return fail("need 0 < lambda_init < lambda_max");
-  if (!(c->lambda_up > 0) || !(c->lambda_down > 0)) return fail("lambda factors must be > 0");
+  // > 1 guarantees the retry loop terminates (lambda reaches lambda_max)
+  if (!(c->lambda_up > 1) || !(c->lambda_down > 1)) return fail("lambda factors must be > 1");
   if (!(c->sigma_min > 0) || !(c->sigma_max > c->sigma_min)) return fail("need 0 < sigma_min < sigma_max");
   if (!(c->margin_x >= 0) || !(c->margin_y >= 0)) return fail("margins must be >= 0");
   k.max_it = c->max_iterations;
@@ -78,28 +79,41 @@ int sm_count_of_current() {
   return sms > 0 ? sms : 1;
 }
 
-int dispatch_fit(int P, int slots, int ppl, const sf::LaunchFit& a) {
+void shape_need(const sf::Geom& g, int* ch, int* tl) {
+  *ch = 0;
+  *tl = 0;
+  for (int l = 0; l < g.lanes; ++l) {
+    *ch = std::max(*ch, (int)g.nc[l]);
+    *tl = std::max(*tl, (int)g.nt[l]);
+  }
+}
+
+int dispatch_fit(int P, const sf::LaunchFit& a) {
   cudaError_t err = cudaSuccess;
-  int used = -1;
+  int used = -1, ch, tl;
+  const int slots = a.geom.slots;
+  shape_need(a.geom, &ch, &tl);
 #define SF_CASE(PP, S) \
-  if (P == PP && slots == S) used = sf::launch_fit_P##PP##_S##S(ppl, a, &err);
+  if (P == PP && slots == S) used = sf::launch_fit_P##PP##_S##S(ch, tl, a, &err);
   SF_CASE(3, 1) SF_CASE(3, 2) SF_CASE(3, 4) SF_CASE(3, 8) SF_CASE(3, 16)
   SF_CASE(4, 1) SF_CASE(4, 2) SF_CASE(4, 4) SF_CASE(4, 8) SF_CASE(4, 16)
 #undef SF_CASE
-  if (used < 0) return fail("no kernel instantiation for P=%d slots=%d ppl=%d", P, slots, ppl);
+  if (used < 0) return fail("no kernel instantiation for P=%d slots=%d chain=%d tail=%d", P, slots, ch, tl);
   if (err != cudaSuccess) return fail("fit kernel launch failed: %s", cudaGetErrorString(err));
   return 0;
 }
 
-int dispatch_eval(int P, int slots, int ppl, const sf::LaunchEval& a) {
+int dispatch_eval(int P, const sf::LaunchEval& a) {
   cudaError_t err = cudaSuccess;
-  int used = -1;
+  int used = -1, ch, tl;
+  const int slots = a.geom.slots;
+  shape_need(a.geom, &ch, &tl);
 #define SF_CASE(PP, S) \
-  if (P == PP && slots == S) used = sf::launch_eval_P##PP##_S##S(ppl, a, &err);
+  if (P == PP && slots == S) used = sf::launch_eval_P##PP##_S##S(ch, tl, a, &err);
   SF_CASE(3, 1) SF_CASE(3, 2) SF_CASE(3, 4) SF_CASE(3, 8) SF_CASE(3, 16)
   SF_CASE(4, 1) SF_CASE(4, 2) SF_CASE(4, 4) SF_CASE(4, 8) SF_CASE(4, 16)
 #undef SF_CASE
-  if (used < 0) return fail("no kernel instantiation for P=%d slots=%d ppl=%d", P, slots, ppl);
+  if (used < 0) return fail("no kernel instantiation for P=%d slots=%d chain=%d tail=%d", P, slots, ch, tl);
   if (err != cudaSuccess) return fail("eval kernel launch failed: %s", cudaGetErrorString(err));
   return 0;
 }
@@ -251,7 +265,7 @@ int run_shard(int dev, HostJob& j) {
   const int64_t total = j.hi - j.lo;
   if (total <= 0) return 0;
   sf::Geom geom;
-  const int ppl = sf::build_geom(j.W, j.H, P, geom);
+  sf::build_geom(j.W, j.H, P, geom);
   sf::Cfg kc;
   if (make_cfg(j.cfg, j.W, j.H, kc) != 0) return -1;
   // chunking: >= 8 chunks for overlap when the shard is large, bounded buffers
@@ -293,7 +307,7 @@ int run_shard(int dev, HostJob& j) {
     a.out = sf::FitOut{s.d_par, s.d_a, s.d_b, s.d_c, s.d_st, s.d_it, c->d_evals};
     a.stream = s.stream;
     a.sm_count = c->sms;
-    if (dispatch_fit(P, geom.slots, ppl, a) != 0) return -1;
+    if (dispatch_fit(P, a) != 0) return -1;
     SF_CUDA(cudaEventRecord(s.ev[2], s.stream));
     if (j.pinned_out) {
       SF_CUDA(cudaMemcpyAsync(j.par + lo * P, s.d_par, n * P * sizeof(float), cudaMemcpyDeviceToHost, s.stream));
@@ -337,6 +351,13 @@ int run_shard(int dev, HostJob& j) {
 extern "C" {
 
 int sf_version(void) { return SF_ABI_VERSION; }
+
+int sf_debug_npexp_device(const float* d_x, float* d_y, int64_t n, int32_t variant, void* stream) {
+  if (n < 0 || (variant != 0 && variant != 1)) return fail("bad arguments");
+  cudaError_t e = sf::launch_npexp(d_x, d_y, n, variant, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail("npexp launch failed: %s", cudaGetErrorString(e));
+  return 0;
+}
 
 int sf_lane_geometry(int32_t width, int32_t height, int32_t* slots, int32_t* ppl, int16_t* nc, int16_t* nt,
                      int16_t* base, int16_t* tbase) {
@@ -390,7 +411,7 @@ int sf_fit_batch_device(const float* d_images, int32_t width, int32_t height, in
   if (!d_images || !d_inits || !d_params || !d_alpha || !d_beta || !d_nchi2 || !d_status || !d_iters)
     return fail("NULL buffer");
   sf::Geom geom;
-  const int ppl = sf::build_geom(width, height, cfg->model, geom);
+  sf::build_geom(width, height, cfg->model, geom);
   sf::LaunchFit a;
   a.images = d_images;
   a.inits = d_inits;
@@ -401,7 +422,7 @@ int sf_fit_batch_device(const float* d_images, int32_t width, int32_t height, in
                      reinterpret_cast<unsigned long long*>(d_evals)};
   a.stream = static_cast<cudaStream_t>(stream);
   a.sm_count = sm_count_of_current();
-  return dispatch_fit(cfg->model, geom.slots, ppl, a);
+  return dispatch_fit(cfg->model, a);
 }
 
 int sf_eval_batch_device(const float* d_images, int32_t width, int32_t height, int64_t count, int32_t model,
@@ -411,7 +432,7 @@ int sf_eval_batch_device(const float* d_images, int32_t width, int32_t height, i
   if (count < 0) return fail("negative count");
   if (count == 0) return 0;
   sf::Geom geom;
-  const int ppl = sf::build_geom(width, height, model, geom);
+  sf::build_geom(width, height, model, geom);
   sf::LaunchEval a;
   a.images = d_images;
   a.params = d_params;
@@ -419,7 +440,7 @@ int sf_eval_batch_device(const float* d_images, int32_t width, int32_t height, i
   a.geom = geom;
   a.out = d_out;
   a.stream = static_cast<cudaStream_t>(stream);
-  return dispatch_eval(model, geom.slots, ppl, a);
+  return dispatch_eval(model, a);
 }
 
 int sf_estimate_initial_device(const float* d_images, int32_t width, int32_t height, int64_t count, int32_t model,

@@ -5,8 +5,8 @@
 // so a group that stops early simply loads its next spot while its warp-mates
 // keep iterating.  Each loop trip is: [refill groups that finished] ->
 // one fused evaluation (sf_device.cuh:evaluate) -> the LM state machine of
-// SURVEY App. A, which is divergent across groups but
-// cheap.  No host round trip happens inside a fit.
+// SURVEY App. A, divergent across groups but cheap.  No
+// host round trip happens inside a fit.
 #pragma once
 #include "sf_device.cuh"
 
@@ -89,7 +89,10 @@ __device__ __forceinline__ bool lm_step(LMState<P>& s, const Eval<P>& E, const C
       s.ab = E.alpha;
       s.bb = E.beta;
 #pragma unroll
-      for (int k = 0; k < P; ++k) { s.best[k] = s.p[k]; s.rhs[k] = E.rhs[k]; }
+      for (int k = 0; k < P; ++k) {
+        s.best[k] = s.p[k];
+        s.rhs[k] = E.rhs[k];
+      }
 #pragma unroll
       for (int m = 0; m < T; ++m) s.jtj[m] = E.jtj[m];
       s.first = true;
@@ -156,61 +159,83 @@ __device__ __forceinline__ bool lm_step(LMState<P>& s, const Eval<P>& E, const C
   }
 }
 
-template <int SLOTS>
-constexpr int threads_per_block() {
-  return SLOTS >= 8 ? 8 * SLOTS : 128;
-}
+// Lane identity and pixel ownership, shared by the fit and eval kernels.
+template <int P, int CH, int TL, int SLOTS>
+struct LaneSetup {
+  int gl;         // lane within the group
+  int64_t gid;    // group id
+  int64_t ngroups;
+  uint32_t own;   // owned-pixel mask, bit j (chain j < CH, tail CH + t)
+  int base, tbase;
 
-template <int P, int PPL, int SLOTS>
-__global__ void __launch_bounds__(threads_per_block<SLOTS>())
+  // pixel index of slot j (chain: base + 8 j, tail: tbase + j - CH), or -1 if not owned
+  __device__ __forceinline__ int off(int j) const {
+    return owns(own, j) ? (j < CH ? base + 8 * j : tbase + (j - CH)) : -1;
+  }
+
+  __device__ __forceinline__ void init(Smem<P, CH, TL, SLOTS>& S, const Geom& geom) {
+    constexpr int LANES = 8 * SLOTS;
+    const int lane = threadIdx.x & 31;
+    if constexpr (SLOTS >= 8) {
+      gl = threadIdx.x;
+      gid = blockIdx.x;
+      ngroups = gridDim.x;
+    } else {
+      constexpr int GPW = 32 / LANES;
+      gl = lane % LANES;
+      gid = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * GPW + lane / LANES;
+      ngroups = (int64_t)gridDim.x * (blockDim.x >> 5) * GPW;
+    }
+    const int nc = geom.nc[gl], nt = geom.nt[gl];
+    base = geom.base[gl];
+    tbase = geom.tbase[gl];
+    own = 0u;
+#pragma unroll
+    for (int j = 0; j < CH + TL; ++j) {
+      const bool o = j < CH ? j < nc : (j - CH) < nt;
+      own |= (o ? 1u : 0u) << j;
+    }
+    // coordinates table: row gl written by the group's lanes of the first group in the CTA
+    if (threadIdx.x < LANES) {
+#pragma unroll
+      for (int j = 0; j < CH + TL; ++j) {
+        const int pp = off(j) < 0 ? 0 : off(j);
+        S.xy[j][gl] = make_float2((float)(pp % geom.W), (float)(pp / geom.W));
+      }
+    }
+    __syncthreads();
+  }
+};
+
+template <int P, int CH, int TL, int SLOTS>
+__global__ void __launch_bounds__(threads_per_block<SLOTS>(), SLOTS >= 8 ? 1 : (P == 4 ? 3 : 4))
     fit_kernel(const float* __restrict__ images, const float* __restrict__ inits, int64_t count, const Geom geom,
                const Cfg cfg, FitOut out) {
-  constexpr int LANES = 8 * SLOTS;
-  __shared__ double sm[kSmemDoubles<SLOTS>];
-  const int lane = threadIdx.x & 31;
-  int gl;
-  int64_t gid, ngroups;
-  if constexpr (SLOTS >= 8) {
-    gl = threadIdx.x;
-    gid = blockIdx.x;
-    ngroups = gridDim.x;
-  } else {
-    constexpr int GPW = 32 / LANES;
-    gl = lane % LANES;
-    gid = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * GPW + lane / LANES;
-    ngroups = (int64_t)gridDim.x * (blockDim.x >> 5) * GPW;
-  }
-  const bool leader = gl == 0;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem<P, CH, TL, SLOTS>& S = *reinterpret_cast<Smem<P, CH, TL, SLOTS>*>(smem_raw);
+  LaneSetup<P, CH, TL, SLOTS> L;
+  L.init(S, geom);
+  const int tid = threadIdx.x;
+  const bool leader = L.gl == 0;
   const int N = geom.N;
-  const int nc = geom.nc[gl], nt = geom.nt[gl];
-  const int base = geom.base[gl], tbase = geom.tbase[gl];
   const double n = (double)N;
 
-  // lane-constant pixel coordinates (model.py:35-41)
-  float xs[PPL], ys[PPL];
-  int off[PPL];
-#pragma unroll
-  for (int j = 0; j < PPL; ++j) {
-    int pix = j < nc ? base + 8 * j : (j < nc + nt ? tbase + (j - nc) : -1);
-    off[j] = pix;
-    const int pp = pix < 0 ? 0 : pix;
-    xs[j] = (float)(pp % geom.W);
-    ys[j] = (float)(pp / geom.W);
-  }
-
-  float g[PPL];
   double G = 0.0;
   LMState<P> s;
-  int64_t spot = gid - ngroups;
+  int64_t spot = L.gid - L.ngroups;
   bool need = true, exhausted = false;
   unsigned n_g = 0, n_t = 0, n_e = 0;
 
 #pragma unroll 1
   for (;;) {
+    // Every warp-collective below (votes, shuffles inside pixel_sum and
+    // evaluate) is reached by all 32 lanes on every trip: groups only diverge
+    // in the LM bookkeeping after the evaluation.
+    bool skip = false;  // group refilled with an InvalidInput spot: no LM step this trip
     if (__any_sync(kFull, need)) {
       // ---- refill: next spot for every group whose fit finished
       if (need) {
-        spot += ngroups;
+        spot += L.ngroups;
         exhausted = spot >= count;
       }
       const bool load = need && !exhausted;
@@ -218,9 +243,11 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>())
       if (load) {
         const float* img = images + spot * (int64_t)N;
 #pragma unroll
-        for (int j = 0; j < PPL; ++j) {
-          g[j] = off[j] >= 0 ? __ldg(img + off[j]) : 0.0f;
-          bad = bad || !isfinite(g[j]);
+        for (int j = 0; j < CH + TL; ++j) {
+          const int o = L.off(j);
+          const float v = o >= 0 ? __ldg(img + o) : 0.0f;
+          S.gv[j][tid] = v;
+          bad = bad || !isfinite(v);
         }
         float init[P];
         double v[P];
@@ -242,25 +269,25 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>())
         }
       }
       const bool gbad = group_any<SLOTS>(bad);
-      const double gsum = pixel_sum<PPL, SLOTS>(g, nc, nt, sm);
+      const double gsum = pixel_sum<P, CH, TL, SLOTS>(S);
       if (load) {
         G = gsum;
         if (gbad) {
           write_result<P>(out, spot, leader, s.p, true, 0.f, 0.f, 0.f, N, SF_STOP_NOT_CONVERGED | SF_FLAG_INVALID, 0);
           need = true;  // fetch the next spot on the next trip
+          skip = true;
         } else {
           need = false;
         }
       } else if (need) {
         need = false;  // exhausted
       }
-      if (load && gbad) continue;
     }
     if (__all_sync(kFull, exhausted)) break;
 
     Eval<P> E;
-    evaluate<P, PPL, SLOTS>(xs, ys, g, nc, nt, G, n, s.p, E, sm);
-    if (!exhausted) {
+    evaluate<P, CH, TL, SLOTS>(S, L.gl, L.own, G, n, s.p, E);
+    if (!exhausted && !skip) {
       n_e += 1;
       if (lm_step<P>(s, E, cfg, out, spot, leader, N, n_g, n_t)) need = true;
     }
@@ -273,61 +300,54 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>())
 }
 
 // Model-level evaluation (sf_eval_batch_device): one group per spot, no LM.
-template <int P, int PPL, int SLOTS>
+template <int P, int CH, int TL, int SLOTS>
 __global__ void __launch_bounds__(threads_per_block<SLOTS>())
     eval_kernel(const float* __restrict__ images, const float* __restrict__ params, int64_t count, const Geom geom,
                 sf_eval_record* __restrict__ out) {
-  constexpr int LANES = 8 * SLOTS;
-  __shared__ double sm[kSmemDoubles<SLOTS>];
-  const int lane = threadIdx.x & 31;
-  int gl;
-  int64_t gid;
-  if constexpr (SLOTS >= 8) {
-    gl = threadIdx.x;
-    gid = blockIdx.x;
-  } else {
-    constexpr int GPW = 32 / LANES;
-    gl = lane % LANES;
-    gid = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * GPW + lane / LANES;
-  }
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem<P, CH, TL, SLOTS>& S = *reinterpret_cast<Smem<P, CH, TL, SLOTS>*>(smem_raw);
+  LaneSetup<P, CH, TL, SLOTS> L;
+  L.init(S, geom);
+  const int tid = threadIdx.x;
   const int N = geom.N;
-  const int nc = geom.nc[gl], nt = geom.nt[gl];
-  const int base = geom.base[gl], tbase = geom.tbase[gl];
-  const bool valid = gid < count;
-  const int64_t spot = valid ? gid : 0;
-  float xs[PPL], ys[PPL], g[PPL];
+  const bool valid = L.gid < count;
+  const int64_t spot = valid ? L.gid : 0;
   const float* img = images + spot * (int64_t)N;
 #pragma unroll
-  for (int j = 0; j < PPL; ++j) {
-    const int pix = j < nc ? base + 8 * j : (j < nc + nt ? tbase + (j - nc) : -1);
-    const int pp = pix < 0 ? 0 : pix;
-    xs[j] = (float)(pp % geom.W);
-    ys[j] = (float)(pp / geom.W);
-    g[j] = (pix >= 0 && valid) ? __ldg(img + pix) : 0.0f;
-  }
+  for (int j = 0; j < CH + TL; ++j) S.gv[j][tid] = (L.off(j) >= 0 && valid) ? __ldg(img + L.off(j)) : 0.0f;
   float pe[P];
 #pragma unroll
   for (int k = 0; k < P; ++k) pe[k] = valid ? __ldg(params + spot * P + k) : 1.0f;
-  const double G = pixel_sum<PPL, SLOTS>(g, nc, nt, sm);
+  const double G = pixel_sum<P, CH, TL, SLOTS>(S);
   Eval<P> E;
   EvalExtras<P> X;
-  evaluate<P, PPL, SLOTS, true>(xs, ys, g, nc, nt, G, (double)N, pe, E, sm, &X);
-  if (valid && gl == 0) {
+  evaluate<P, CH, TL, SLOTS, true>(S, L.gl, L.own, G, (double)N, pe, E, &X);
+  if (valid && L.gl == 0) {
     sf_eval_record r;
     r.singular = E.singular ? 1 : 0;
-    r.alpha = E.alpha; r.beta = E.beta; r.chi = E.chi;
-    r.F = X.F; r.G = G; r.FF = X.FF; r.FG = X.FG; r.denom = X.denom;
+    r.alpha = E.alpha;
+    r.beta = E.beta;
+    r.chi = E.chi;
+    r.F = X.F;
+    r.G = G;
+    r.FF = X.FF;
+    r.FG = X.FG;
+    r.denom = X.denom;
+#pragma unroll
     for (int k = 0; k < 4; ++k) {
+      const int kk = k < P ? k : 0;
       const bool in = k < P;
-      r.dF[k] = in ? X.dF[k < P ? k : 0] : 0.0;
-      r.dFF[k] = in ? X.dFF[k < P ? k : 0] : 0.0;
-      r.dFG[k] = in ? X.dFG[k < P ? k : 0] : 0.0;
-      r.gamma[k] = in ? X.gamma[k < P ? k : 0] : 0.0;
-      r.dalpha[k] = in ? X.dalpha[k < P ? k : 0] : 0.0;
-      r.dbeta[k] = in ? X.dbeta[k < P ? k : 0] : 0.0;
-      r.rhs[k] = in ? E.rhs[k < P ? k : 0] : 0.0;
+      r.dF[k] = in ? X.dF[kk] : 0.0;
+      r.dFF[k] = in ? X.dFF[kk] : 0.0;
+      r.dFG[k] = in ? X.dFG[kk] : 0.0;
+      r.gamma[k] = in ? X.gamma[kk] : 0.0;
+      r.dalpha[k] = in ? X.dalpha[kk] : 0.0;
+      r.dbeta[k] = in ? X.dbeta[kk] : 0.0;
+      r.rhs[k] = in ? E.rhs[kk] : 0.0;
     }
-    for (int m = 0; m < 10; ++m) r.jtj[m] = m < P * (P + 1) / 2 ? E.jtj[m < P * (P + 1) / 2 ? m : 0] : 0.0;
+    constexpr int T = P * (P + 1) / 2;
+#pragma unroll
+    for (int m = 0; m < 10; ++m) r.jtj[m] = m < T ? E.jtj[m < T ? m : 0] : 0.0;
     out[spot] = r;
   }
 }

@@ -33,8 +33,9 @@ inline void pw_place(int n, int start, int slot, int span, std::vector<Leaf>& ou
   pw_place(n - n2, start + n2, slot + span / 2, span / 2, out);
 }
 
-// Returns the pixels-per-lane requirement; fills g.  N must be in [1, 1024].
-inline int build_geom(int W, int H, int P, Geom& g) {
+// Fills g; returns the pixels-per-lane requirement and, through ch_need /
+// tl_need, the largest chain and tail pixel counts of any lane.  N in [1, 1024].
+inline int build_geom(int W, int H, int P, Geom& g, int* ch_need = nullptr, int* tl_need = nullptr) {
   std::memset(&g, 0, sizeof(g));
   g.W = W;
   g.H = H;
@@ -45,7 +46,7 @@ inline int build_geom(int W, int H, int P, Geom& g) {
   g.lanes = 8 * g.slots;
   std::vector<Leaf> leaves;
   pw_place(g.N, 0, 0, g.slots, leaves);
-  int ppl = 1;
+  int ppl = 1, chn = 0, tln = 0;
   for (const Leaf& L : leaves) {
     const int nc = L.m >= 8 ? L.m / 8 : 0;
     const int nt = L.m >= 8 ? L.m % 8 : L.m;
@@ -57,7 +58,11 @@ inline int build_geom(int W, int H, int P, Geom& g) {
       g.tbase[lane] = (int16_t)(L.start + 8 * nc);
     }
     ppl = std::max(ppl, nc + nt);
+    chn = std::max(chn, nc);
+    tln = std::max(tln, nt);
   }
+  if (ch_need) *ch_need = chn;
+  if (tl_need) *tl_need = tln;
   return ppl;
 }
 

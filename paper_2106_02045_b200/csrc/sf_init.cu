@@ -85,4 +85,17 @@ cudaError_t launch_estimate_initial(const float* images, int W, int H, int64_t c
   return cudaGetLastError();
 }
 
+// Exhaustive-check helper: numpy exp on the device (variant 0: production
+// npexp, 1: the same with CUDA's IEEE __fdiv_rn).
+__global__ void npexp_kernel(const float* __restrict__ x, float* __restrict__ y, int64_t n, int variant) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = variant == 0 ? npexp(x[i]) : npexp_ieee_div(x[i]);
+}
+
+cudaError_t launch_npexp(const float* x, float* y, int64_t n, int variant, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  npexp_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(x, y, n, variant);
+  return cudaGetLastError();
+}
+
 }  // namespace sf

@@ -28,11 +28,11 @@ struct LaunchEval {
   cudaStream_t stream;
 };
 
-// Each returns the PPL instantiation used (>= ppl_needed), or -1 if none fits;
-// a CUDA launch error is reported through *err.
-#define SF_DECLARE_UNIT(P, S)                                                      \
-  int launch_fit_P##P##_S##S(int ppl_needed, const LaunchFit& a, cudaError_t* err); \
-  int launch_eval_P##P##_S##S(int ppl_needed, const LaunchEval& a, cudaError_t* err);
+// Each returns the (CH*16 + TL) instantiation used, or -1 if none fits; a CUDA
+// launch error is reported through *err.
+#define SF_DECLARE_UNIT(P, S)                                                                      \
+  int launch_fit_P##P##_S##S(int ch_need, int tl_need, const LaunchFit& a, cudaError_t* err);      \
+  int launch_eval_P##P##_S##S(int ch_need, int tl_need, const LaunchEval& a, cudaError_t* err);
 SF_DECLARE_UNIT(3, 1)
 SF_DECLARE_UNIT(3, 2)
 SF_DECLARE_UNIT(3, 4)
@@ -48,5 +48,8 @@ SF_DECLARE_UNIT(4, 16)
 // initializer kernel launcher (sf_init.cu)
 cudaError_t launch_estimate_initial(const float* images, int W, int H, int64_t count, int P, double sigma_min,
                                     double sigma_max, float* inits, float* amps, cudaStream_t stream);
+
+// exhaustive-check helper (sf_init.cu)
+cudaError_t launch_npexp(const float* x, float* y, int64_t n, int variant, cudaStream_t stream);
 
 }  // namespace sf

@@ -66,6 +66,8 @@ class FitConfig:
             raise ValueError("thresholds must be > 0 (max_error >= 0)")
         if not 0 < self.lambda_init < self.lambda_max:
             raise ValueError("need 0 < lambda_init < lambda_max")
+        if not (self.lambda_up > 1 and self.lambda_down > 1):
+            raise ValueError("lambda factors must be > 1")
 
     def resolved_bounds(self, grid: PixelGrid) -> ParameterBounds:
         return self.bounds if self.bounds is not None else ParameterBounds.for_grid(grid)
