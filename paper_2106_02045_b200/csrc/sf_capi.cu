@@ -90,11 +90,10 @@ void shape_need(const sf::Geom& g, int* ch, int* tl) {
 
 int dispatch_fit(int P, const sf::LaunchFit& a) {
   cudaError_t err = cudaSuccess;
-  int used = -1, ch, tl;
-  const int slots = a.geom.slots;
-  shape_need(a.geom, &ch, &tl);
+  int used = -1;
+  const int slots = a.geom.slots, ch = a.geom.ch, tl = a.geom.tl;
 #define SF_CASE(PP, S) \
-  if (P == PP && slots == S) used = sf::launch_fit_P##PP##_S##S(ch, tl, a, &err);
+  if (P == PP && slots == S) used = sf::launch_fit_P##PP##_S##S(a, &err);
   SF_CASE(3, 1) SF_CASE(3, 2) SF_CASE(3, 4) SF_CASE(3, 8) SF_CASE(3, 16)
   SF_CASE(4, 1) SF_CASE(4, 2) SF_CASE(4, 4) SF_CASE(4, 8) SF_CASE(4, 16)
 #undef SF_CASE
@@ -105,11 +104,10 @@ int dispatch_fit(int P, const sf::LaunchFit& a) {
 
 int dispatch_eval(int P, const sf::LaunchEval& a) {
   cudaError_t err = cudaSuccess;
-  int used = -1, ch, tl;
-  const int slots = a.geom.slots;
-  shape_need(a.geom, &ch, &tl);
+  int used = -1;
+  const int slots = a.geom.slots, ch = a.geom.ch, tl = a.geom.tl;
 #define SF_CASE(PP, S) \
-  if (P == PP && slots == S) used = sf::launch_eval_P##PP##_S##S(ch, tl, a, &err);
+  if (P == PP && slots == S) used = sf::launch_eval_P##PP##_S##S(a, &err);
   SF_CASE(3, 1) SF_CASE(3, 2) SF_CASE(3, 4) SF_CASE(3, 8) SF_CASE(3, 16)
   SF_CASE(4, 1) SF_CASE(4, 2) SF_CASE(4, 4) SF_CASE(4, 8) SF_CASE(4, 16)
 #undef SF_CASE

@@ -65,7 +65,9 @@ __device__ __forceinline__ bool lm_step(LMState<P>& s, const Eval<P>& E, const C
   constexpr int T = P * (P + 1) / 2;
   float chit = 0.0f;
   bool small = s.small;
-  int action;  // 0: process E as G-eval, 1: solve a trial, 2: post-trial decision
+  int status = -1;       // StopReason | flags once the fit has finished
+  bool at_best = false;  // result is the saved best point (restore) rather than E's point
+  int action;            // 0: process E as G-eval, 1: solve a trial, 2: post-trial decision
   if (s.trial) {
     chit = E.singular ? __int_as_float(0x7fc00000) : E.chi;
     action = 2;
@@ -78,12 +80,12 @@ __device__ __forceinline__ bool lm_step(LMState<P>& s, const Eval<P>& E, const C
       s.it += 1;
       n_g += 1;
       if (E.singular || !isfinite(E.chi)) {
-        write_result<P>(o, spot, leader, s.p, E.singular, E.chi, E.alpha, E.beta, n_pix, SF_STOP_NOT_CONVERGED, s.it);
-        return true;
+        status = SF_STOP_NOT_CONVERGED;
+        break;
       }
       if ((double)E.chi < c.max_error) {
-        write_result<P>(o, spot, leader, s.p, false, E.chi, E.alpha, E.beta, n_pix, SF_STOP_MAX_ERROR, s.it);
-        return true;
+        status = SF_STOP_MAX_ERROR;
+        break;
       }
       s.chib = E.chi;
       s.ab = E.alpha;
@@ -129,51 +131,58 @@ __device__ __forceinline__ bool lm_step(LMState<P>& s, const Eval<P>& E, const C
       continue;
     }
     if (isnan(chit) || (s.chib < chit && s.lam >= c.lam_max)) {
-      write_result<P>(o, spot, leader, s.best, false, s.chib, s.ab, s.bb, n_pix, SF_STOP_NOT_CONVERGED, s.it);
-      return true;
+      status = SF_STOP_NOT_CONVERGED;
+      at_best = true;
+      break;
     }
     if (s.chib < chit) {
-      write_result<P>(o, spot, leader, s.best, false, s.chib, s.ab, s.bb, n_pix, SF_STOP_MIN_DELTA | SF_FLAG_NOIMP,
-                      s.it);
-      return true;
+      status = SF_STOP_MIN_DELTA | SF_FLAG_NOIMP;
+      at_best = true;
+      break;
     }
     if ((double)chit < c.max_error) {
-      write_result<P>(o, spot, leader, s.p, false, E.chi, E.alpha, E.beta, n_pix, SF_STOP_MAX_ERROR, s.it);
-      return true;
+      status = SF_STOP_MAX_ERROR;
+      break;
     }
     if ((double)s.chib * (1.0 - c.min_delta) < (double)chit) {
-      write_result<P>(o, spot, leader, s.p, false, E.chi, E.alpha, E.beta, n_pix, SF_STOP_MIN_DELTA, s.it);
-      return true;
+      status = SF_STOP_MIN_DELTA;
+      break;
     }
     if (small) {
-      write_result<P>(o, spot, leader, s.p, false, E.chi, E.alpha, E.beta, n_pix, SF_STOP_MIN_STEP, s.it);
-      return true;
+      status = SF_STOP_MIN_STEP;
+      break;
     }
     if (s.it >= c.max_it) {
-      write_result<P>(o, spot, leader, s.p, false, E.chi, E.alpha, E.beta, n_pix, SF_STOP_MAX_ITERATIONS, s.it);
-      return true;
+      status = SF_STOP_MAX_ITERATIONS;
+      break;
     }
     // accepted, budget left: E is exactly the next iteration's G-eval at s.p
     s.trial = false;
     action = 0;
   }
+  float rp[P];
+#pragma unroll
+  for (int k = 0; k < P; ++k) rp[k] = at_best ? s.best[k] : s.p[k];
+  write_result<P>(o, spot, leader, rp, !at_best && E.singular, at_best ? s.chib : E.chi, at_best ? s.ab : E.alpha,
+                  at_best ? s.bb : E.beta, n_pix, status, s.it);
+  return true;
 }
 
 // Lane identity and pixel ownership, shared by the fit and eval kernels.
-template <int P, int CH, int TL, int SLOTS>
+template <int P, int SLOTS>
 struct LaneSetup {
   int gl;         // lane within the group
   int64_t gid;    // group id
   int64_t ngroups;
-  uint32_t own;   // owned-pixel mask, bit j (chain j < CH, tail CH + t)
-  int base, tbase;
+  uint32_t own;   // owned-pixel mask, bit j (chain j < ch, tail ch + t)
+  int base, tbase, ch, tl;
 
-  // pixel index of slot j (chain: base + 8 j, tail: tbase + j - CH), or -1 if not owned
+  // pixel index of slot j (chain: base + 8 j, tail: tbase + j - ch), or -1 if not owned
   __device__ __forceinline__ int off(int j) const {
-    return owns(own, j) ? (j < CH ? base + 8 * j : tbase + (j - CH)) : -1;
+    return owns(own, j) ? (j < ch ? base + 8 * j : tbase + (j - ch)) : -1;
   }
 
-  __device__ __forceinline__ void init(Smem<P, CH, TL, SLOTS>& S, const Geom& geom) {
+  __device__ __forceinline__ void init(Smem<P, SLOTS>& S, const Geom& geom) {
     constexpr int LANES = 8 * SLOTS;
     const int lane = threadIdx.x & 31;
     if constexpr (SLOTS >= 8) {
@@ -186,34 +195,35 @@ struct LaneSetup {
       gid = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * GPW + lane / LANES;
       ngroups = (int64_t)gridDim.x * (blockDim.x >> 5) * GPW;
     }
+    ch = geom.ch;
+    tl = geom.tl;
     const int nc = geom.nc[gl], nt = geom.nt[gl];
     base = geom.base[gl];
     tbase = geom.tbase[gl];
     own = 0u;
-#pragma unroll
-    for (int j = 0; j < CH + TL; ++j) {
-      const bool o = j < CH ? j < nc : (j - CH) < nt;
+    for (int j = 0; j < ch + tl; ++j) {
+      const bool o = j < ch ? j < nc : (j - ch) < nt;
       own |= (o ? 1u : 0u) << j;
     }
-    // coordinates table: row gl written by the group's lanes of the first group in the CTA
+    // coordinates table: rows written by the lanes of the CTA's first group
     if (threadIdx.x < LANES) {
-#pragma unroll
-      for (int j = 0; j < CH + TL; ++j) {
+      for (int j = 0; j < ch + tl; ++j) {
         const int pp = off(j) < 0 ? 0 : off(j);
-        S.xy[j][gl] = make_float2((float)(pp % geom.W), (float)(pp / geom.W));
+        S.row[j].xy[gl] = make_float2((float)(pp % geom.W), (float)(pp / geom.W));
       }
     }
     __syncthreads();
   }
 };
 
-template <int P, int CH, int TL, int SLOTS>
+template <int P, int SLOTS>
 __global__ void __launch_bounds__(threads_per_block<SLOTS>(), SLOTS >= 8 ? 1 : (P == 4 ? 3 : 4))
     fit_kernel(const float* __restrict__ images, const float* __restrict__ inits, int64_t count, const Geom geom,
                const Cfg cfg, FitOut out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  Smem<P, CH, TL, SLOTS>& S = *reinterpret_cast<Smem<P, CH, TL, SLOTS>*>(smem_raw);
-  LaneSetup<P, CH, TL, SLOTS> L;
+  Smem<P, SLOTS> S;
+  S.bind(smem_raw);
+  LaneSetup<P, SLOTS> L;
   L.init(S, geom);
   const int tid = threadIdx.x;
   const bool leader = L.gl == 0;
@@ -242,11 +252,11 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(), SLOTS >= 8 ? 1 : (
       bool bad = false;
       if (load) {
         const float* img = images + spot * (int64_t)N;
-#pragma unroll
-        for (int j = 0; j < CH + TL; ++j) {
+#pragma unroll 4
+        for (int j = 0; j < L.ch + L.tl; ++j) {
           const int o = L.off(j);
           const float v = o >= 0 ? __ldg(img + o) : 0.0f;
-          S.gv[j][tid] = v;
+          S.row[j].gv[tid] = v;
           bad = bad || !isfinite(v);
         }
         float init[P];
@@ -269,7 +279,7 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(), SLOTS >= 8 ? 1 : (
         }
       }
       const bool gbad = group_any<SLOTS>(bad);
-      const double gsum = pixel_sum<P, CH, TL, SLOTS>(S);
+      const double gsum = pixel_sum<P, SLOTS>(S, L.ch, L.tl);
       if (load) {
         G = gsum;
         if (gbad) {
@@ -286,7 +296,7 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(), SLOTS >= 8 ? 1 : (
     if (__all_sync(kFull, exhausted)) break;
 
     Eval<P> E;
-    evaluate<P, CH, TL, SLOTS>(S, L.gl, L.own, G, n, s.p, E);
+    evaluate<P, SLOTS>(S, L.gl, L.own, L.ch, L.tl, G, n, s.p, E);
     if (!exhausted && !skip) {
       n_e += 1;
       if (lm_step<P>(s, E, cfg, out, spot, leader, N, n_g, n_t)) need = true;
@@ -300,28 +310,28 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(), SLOTS >= 8 ? 1 : (
 }
 
 // Model-level evaluation (sf_eval_batch_device): one group per spot, no LM.
-template <int P, int CH, int TL, int SLOTS>
+template <int P, int SLOTS>
 __global__ void __launch_bounds__(threads_per_block<SLOTS>())
     eval_kernel(const float* __restrict__ images, const float* __restrict__ params, int64_t count, const Geom geom,
                 sf_eval_record* __restrict__ out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  Smem<P, CH, TL, SLOTS>& S = *reinterpret_cast<Smem<P, CH, TL, SLOTS>*>(smem_raw);
-  LaneSetup<P, CH, TL, SLOTS> L;
+  Smem<P, SLOTS> S;
+  S.bind(smem_raw);
+  LaneSetup<P, SLOTS> L;
   L.init(S, geom);
   const int tid = threadIdx.x;
   const int N = geom.N;
   const bool valid = L.gid < count;
   const int64_t spot = valid ? L.gid : 0;
   const float* img = images + spot * (int64_t)N;
-#pragma unroll
-  for (int j = 0; j < CH + TL; ++j) S.gv[j][tid] = (L.off(j) >= 0 && valid) ? __ldg(img + L.off(j)) : 0.0f;
+  for (int j = 0; j < L.ch + L.tl; ++j) S.row[j].gv[tid] = (L.off(j) >= 0 && valid) ? __ldg(img + L.off(j)) : 0.0f;
   float pe[P];
 #pragma unroll
   for (int k = 0; k < P; ++k) pe[k] = valid ? __ldg(params + spot * P + k) : 1.0f;
-  const double G = pixel_sum<P, CH, TL, SLOTS>(S);
+  const double G = pixel_sum<P, SLOTS>(S, L.ch, L.tl);
   Eval<P> E;
   EvalExtras<P> X;
-  evaluate<P, CH, TL, SLOTS, true>(S, L.gl, L.own, G, (double)N, pe, E, &X);
+  evaluate<P, SLOTS, true>(S, L.gl, L.own, L.ch, L.tl, G, (double)N, pe, E, &X);
   if (valid && L.gl == 0) {
     sf_eval_record r;
     r.singular = E.singular ? 1 : 0;

@@ -61,6 +61,8 @@ inline int build_geom(int W, int H, int P, Geom& g, int* ch_need = nullptr, int*
     chn = std::max(chn, nc);
     tln = std::max(tln, nt);
   }
+  g.ch = chn;
+  g.tl = tln;
   if (ch_need) *ch_need = chn;
   if (tl_need) *tl_need = tln;
   return ppl;

@@ -28,11 +28,10 @@ struct LaunchEval {
   cudaStream_t stream;
 };
 
-// Each returns the (CH*16 + TL) instantiation used, or -1 if none fits; a CUDA
-// launch error is reported through *err.
-#define SF_DECLARE_UNIT(P, S)                                                                      \
-  int launch_fit_P##P##_S##S(int ch_need, int tl_need, const LaunchFit& a, cudaError_t* err);      \
-  int launch_eval_P##P##_S##S(int ch_need, int tl_need, const LaunchEval& a, cudaError_t* err);
+// Each returns the number of CTAs launched; a CUDA error is reported through *err.
+#define SF_DECLARE_UNIT(P, S)                                          \
+  int launch_fit_P##P##_S##S(const LaunchFit& a, cudaError_t* err);   \
+  int launch_eval_P##P##_S##S(const LaunchEval& a, cudaError_t* err);
 SF_DECLARE_UNIT(3, 1)
 SF_DECLARE_UNIT(3, 2)
 SF_DECLARE_UNIT(3, 4)
