@@ -22,15 +22,17 @@ struct FitOut {
   unsigned long long* evals;  // [3]: reference G-evals, reference T-evals, fused kernel evals (or null)
 };
 
-// Per-spot LM state, replicated in every lane of the group.
+// Per-spot LM state, replicated in every lane of the group.  The normal system
+// at `best` (needed again only for lambda retries) lives in the group's shared
+// slot `sys`: every lane writes the identical values and reads back only its
+// own writes, so no synchronisation is needed.
 template <int P>
 struct LMState {
   float p[P];     // parameters under evaluation (G point or trial point)
   float best[P];  // PAPER.md:144 "best := current"
-  double delta[P];
   double lam;
-  double jtj[P * (P + 1) / 2], rhs[P];  // normal system at best
-  float chib, ab, bb;                   // chi^2, alpha, beta at best
+  double* sys;    // [T + P]: JtJ (upper packed) then rhs at best
+  float chib, ab, bb;  // chi^2, alpha, beta at best
   int it;
   bool trial, first, small;
 };
@@ -93,22 +95,27 @@ __device__ __forceinline__ bool lm_step(LMState<P>& s, const Eval<P>& E, const C
 #pragma unroll
       for (int k = 0; k < P; ++k) {
         s.best[k] = s.p[k];
-        s.rhs[k] = E.rhs[k];
+        s.sys[T + k] = E.rhs[k];
       }
 #pragma unroll
-      for (int m = 0; m < T; ++m) s.jtj[m] = E.jtj[m];
+      for (int m = 0; m < T; ++m) s.sys[m] = E.jtj[m];
       s.first = true;
       action = 1;
     }
     if (action == 1) {  // PAPER.md:147-151 (and the retry body 159-164)
-      if (solve_step<P>(s.jtj, s.rhs, s.lam, s.delta)) {
+      double jtj[T], rhs[P], delta[P];
+#pragma unroll
+      for (int m = 0; m < T; ++m) jtj[m] = s.sys[m];
+#pragma unroll
+      for (int k = 0; k < P; ++k) rhs[k] = s.sys[T + k];
+      if (solve_step<P>(jtj, rhs, s.lam, delta)) {
         double v[P];
         small = true;
 #pragma unroll
         for (int k = 0; k < P; ++k) {
-          v[k] = (double)s.best[k] + s.delta[k];
+          v[k] = (double)s.best[k] + delta[k];
           const double thr = c.min_step * fmax(fabs((double)s.best[k]), 1.0);
-          small = small && (fabs(s.delta[k]) < thr);
+          small = small && (fabs(delta[k]) < thr);
         }
         limit_params<P>(c, v, s.p);
         s.small = small;
@@ -232,9 +239,32 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(), SLOTS >= 8 ? 1 : (
 
   double G = 0.0;
   LMState<P> s;
+  {
+    constexpr int LANES = 8 * SLOTS;
+    const int gib = SLOTS >= 8 ? 0 : (threadIdx.x >> 5) * (32 / LANES) + (threadIdx.x & 31) / LANES;
+    s.sys = S.sys[gib];
+  }
   int64_t spot = L.gid - L.ngroups;
   bool need = true, exhausted = false;
   unsigned n_g = 0, n_t = 0, n_e = 0;
+
+  // Next-spot prefetch: the pixels land in PixRow::gpre via cp.async while the
+  // current spot iterates, the init in registers; consumed at the next refill.
+  float nxt[P];
+  auto prefetch = [&](int64_t sp) {
+    if (sp < count) {
+      const float* img = images + sp * (int64_t)N;
+#pragma unroll 4
+      for (int j = 0; j < L.ch + L.tl; ++j) {
+        const int o = L.off(j);
+        if (o >= 0) cp_async4(&S.row[j].gpre[tid], img + o);
+      }
+#pragma unroll
+      for (int k = 0; k < P; ++k) nxt[k] = __ldg(inits + sp * P + k);
+    }
+    cp_async_commit();
+  };
+  prefetch(L.gid);
 
 #pragma unroll 1
   for (;;) {
@@ -251,11 +281,10 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(), SLOTS >= 8 ? 1 : (
       const bool load = need && !exhausted;
       bool bad = false;
       if (load) {
-        const float* img = images + spot * (int64_t)N;
+        cp_async_wait_all();  // this lane's prefetched pixels of `spot` have landed
 #pragma unroll 4
         for (int j = 0; j < L.ch + L.tl; ++j) {
-          const int o = L.off(j);
-          const float v = o >= 0 ? __ldg(img + o) : 0.0f;
+          const float v = L.off(j) >= 0 ? S.row[j].gpre[tid] : 0.0f;
           S.row[j].gv[tid] = v;
           bad = bad || !isfinite(v);
         }
@@ -263,10 +292,11 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(), SLOTS >= 8 ? 1 : (
         double v[P];
 #pragma unroll
         for (int k = 0; k < P; ++k) {
-          init[k] = __ldg(inits + spot * P + k);
+          init[k] = nxt[k];
           bad = bad || !isfinite(init[k]);
           v[k] = (double)init[k];
         }
+        prefetch(spot + L.ngroups);
         limit_params<P>(cfg, v, s.p);  // SPEC.md:211 "sigma within bounds after limit"
         s.lam = cfg.lam0;
         s.it = 0;
