@@ -245,23 +245,54 @@ def fit_batch_arrays(m, images: np.ndarray, inits: np.ndarray, W: int, H: int, c
     return out
 
 
-def _worker(args):
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+REF_INSTALL = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+
+
+def model_backend(name: str = "auto"):
+    """The arithmetic under the LM loop: the unmodified reference ``spotfit.model``
+    pip-installed into baseline/_ref when present ("reference"),
+    else the restatement oracle/model_np.py ("port").  Returns (module, kind)."""
+    if name in ("auto", "reference"):
+        import sys
+
+        if os.path.isdir(os.path.join(REF_INSTALL, "spotfit")):
+            if REF_INSTALL not in sys.path:
+                sys.path.insert(0, REF_INSTALL)
+            from spotfit import model as ref_model
+
+            return ref_model, "reference"
+        if name == "reference":
+            raise ImportError(f"reference spotfit not installed under {REF_INSTALL}")
     from oracle import model_np
 
-    images, inits, W, H, cfg = args
-    return fit_batch_arrays(model_np, images, inits, W, H, cfg)
+    return model_np, "port"
 
 
-def fit_batch_parallel(images: np.ndarray, inits: np.ndarray, W: int, H: int, cfg: LMConfig, workers: int = 0):
-    """SPEC.md:381-399: contiguous chunks over a process pool, order preserved."""
+def _worker(args):
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    images, inits, W, H, cfg, backend = args
+    m, _ = model_backend(backend)
+    return fit_batch_arrays(m, images, inits, W, H, cfg)
+
+
+_POOLS = {}
+
+
+def _pool(workers: int):
+    """Persistent worker pool (process start-up stays out of timed batches)."""
     import multiprocessing as mp
 
+    if workers not in _POOLS:
+        _POOLS[workers] = mp.get_context("fork").Pool(workers)
+    return _POOLS[workers]
+
+
+def fit_batch_parallel(images: np.ndarray, inits: np.ndarray, W: int, H: int, cfg: LMConfig, workers: int = 0,
+                       backend: str = "auto"):
+    """SPEC.md:381-399: contiguous chunks over a process pool, order preserved."""
     workers = workers or len(os.sched_getaffinity(0))
     count = inits.shape[0]
     bounds = [(count * w // workers, count * (w + 1) // workers) for w in range(workers)]
-    chunks = [(images[a:b], inits[a:b], W, H, cfg) for a, b in bounds if b > a]
-    ctx = mp.get_context("fork")
-    with ctx.Pool(len(chunks)) as pool:
-        parts = pool.map(_worker, chunks)
+    chunks = [(images[a:b], inits[a:b], W, H, cfg, backend) for a, b in bounds if b > a]
+    parts = _pool(workers).map(_worker, chunks)
     return {k: np.concatenate([p[k] for p in parts]) for k in parts[0]}

@@ -11,7 +11,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libspotfit_b200.so")
+# SPOTFIT_LIB selects an alternative in-tree build (tools/variants: A/B experiments)
+LIB_PATH = os.environ.get("SPOTFIT_LIB") or os.path.join(_HERE, "_lib", "libspotfit_b200.so")
 
 SF_STOP_MAX_ERROR = 0
 SF_STOP_MIN_DELTA = 1

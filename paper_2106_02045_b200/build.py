@@ -55,22 +55,27 @@ def _run(cmd, log):
     return p.stderr
 
 
-def build(force: bool = False, jobs: int = 0, verbose: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
-    os.makedirs(LIBDIR, exist_ok=True)
+def build(force: bool = False, jobs: int = 0, verbose: bool = False, variant: str = "", defines=()) -> str:
+    """Build the library; `variant` + `defines` produce an A/B build under
+    _lib/variants/<variant>/ (select it at run time with SPOTFIT_LIB)."""
+    obj = os.path.join(OBJ, "variants", variant) if variant else OBJ
+    lib = os.path.join(LIBDIR, "variants", variant, "libspotfit_b200.so") if variant else LIB
+    os.makedirs(obj, exist_ok=True)
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
+    dflags = [f"-D{d}" for d in defines]
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(INCLUDE, "spotfit.h"), __file__]
     tasks = []
     for p, s in UNITS:
         src = os.path.join(CSRC, "sf_inst.cu")
-        out = os.path.join(OBJ, f"sf_inst_P{p}_S{s}.o")
-        cmd = [nvcc()] + NVCC_FLAGS + [f"-DSF_P={p}", f"-DSF_SLOTS={s}", "-c", src, "-o", out]
+        out = os.path.join(obj, f"sf_inst_P{p}_S{s}.o")
+        cmd = [nvcc()] + NVCC_FLAGS + dflags + [f"-DSF_P={p}", f"-DSF_SLOTS={s}", "-c", src, "-o", out]
         tasks.append((out, [src] + hdrs, cmd))
     for name in ("sf_init.cu", "sf_capi.cu"):
         src = os.path.join(CSRC, name)
-        out = os.path.join(OBJ, name.replace(".cu", ".o"))
-        tasks.append((out, [src] + hdrs, [nvcc()] + NVCC_FLAGS + ["-c", src, "-o", out]))
+        out = os.path.join(obj, name.replace(".cu", ".o"))
+        tasks.append((out, [src] + hdrs, [nvcc()] + NVCC_FLAGS + dflags + ["-c", src, "-o", out]))
     src = os.path.join(CSRC, "sf_sim.cpp")
-    out = os.path.join(OBJ, "sf_sim.o")
+    out = os.path.join(obj, "sf_sim.o")
     tasks.append((out, [src, os.path.join(INCLUDE, "spotfit.h"), __file__],
                   ["g++", "-O2", "-fPIC", "-std=c++17", "-ffp-contract=off", "-pthread", f"-I{INCLUDE}", "-c", src,
                    "-o", out]))
@@ -83,10 +88,10 @@ def build(force: bool = False, jobs: int = 0, verbose: bool = False) -> str:
                 if verbose:
                     sys.stderr.write(err)
     objs = [t[0] for t in tasks]
-    if force or todo or _stale(LIB, objs):
-        _run([nvcc()] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs + ["-lpthread"],
-             os.path.join(OBJ, "link.log"))
-    return LIB
+    if force or todo or _stale(lib, objs):
+        _run([nvcc()] + ARCH + ["-shared", "-cudart", "static", "-o", lib] + objs + ["-lpthread"],
+             os.path.join(obj, "link.log"))
+    return lib
 
 
 def main(argv=None):
@@ -94,8 +99,10 @@ def main(argv=None):
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--jobs", type=int, default=0)
     ap.add_argument("-v", "--verbose", action="store_true")
+    ap.add_argument("--variant", default="")
+    ap.add_argument("-D", dest="defines", action="append", default=[])
     a = ap.parse_args(argv)
-    print(build(force=a.force, jobs=a.jobs, verbose=a.verbose))
+    print(build(force=a.force, jobs=a.jobs, verbose=a.verbose, variant=a.variant, defines=a.defines))
 
 
 if __name__ == "__main__":

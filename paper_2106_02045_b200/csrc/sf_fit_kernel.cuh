@@ -224,7 +224,7 @@ struct LaneSetup {
 };
 
 template <int P, int SLOTS>
-__global__ void __launch_bounds__(threads_per_block<SLOTS>(), SLOTS >= 8 ? 1 : (P == 4 ? 3 : 4))
+__global__ void __launch_bounds__(threads_per_block<SLOTS>(), SLOTS >= 8 ? 1 : (P == 4 ? SF_MINB_P4 : SF_MINB_P3))
     fit_kernel(const float* __restrict__ images, const float* __restrict__ inits, int64_t count, const Geom geom,
                const Cfg cfg, FitOut out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
