@@ -181,6 +181,78 @@ def run_reference(args):
     return 0
 
 
+def realtime(args, dev):
+    """C5 real-time mode (BASELINE.json configs[4]): 50 spots/frame, 1000 frames,
+    per-frame latency of host frame -> H2D -> GPU initializer -> LM fit -> D2H,
+    replayed as one CUDA graph per frame (host clock around each blocking frame)."""
+    import ctypes
+
+    import torch
+
+    import paper_2106_02045_b200 as sf
+    from paper_2106_02045_b200 import _lib
+
+    W = H = 15
+    spf, frames = args.rt_spots, args.rt_frames
+    grid = sf.PixelGrid(W, H)
+    cfg = sf.FitConfig()
+    ccfg = cfg.to_c(grid, 3)
+    b = cfg.resolved_bounds(grid)
+    L = _lib.lib()
+    allimg = make_workload(W, H, spf * frames, 3, seed=4242).reshape(frames, spf, W * H)
+    pin_in = torch.empty((spf, W * H), dtype=torch.float32).pin_memory()
+    pin_out = torch.empty((spf, 3 + 3), dtype=torch.float32).pin_memory()
+    pin_u8 = torch.empty((2, spf), dtype=torch.uint8).pin_memory()
+    d_img = torch.empty((spf, W * H), dtype=torch.float32, device=dev)
+    d_ini = torch.empty((spf, 3), dtype=torch.float32, device=dev)
+    d_out = torch.empty((spf, 6), dtype=torch.float32, device=dev)
+    d_u8 = torch.empty((2, spf), dtype=torch.uint8, device=dev)
+    d_ab = torch.empty((3, spf), dtype=torch.float32, device=dev)
+    stream = torch.cuda.Stream(dev)
+
+    def frame_ops():
+        st = torch.cuda.current_stream(dev).cuda_stream
+        d_img.copy_(pin_in, non_blocking=True)
+        _lib.check(L.sf_estimate_initial_device(d_img.data_ptr(), W, H, spf, 3, b.sigma_min, b.sigma_max,
+                                                d_ini.data_ptr(), None, st))
+        _lib.check(L.sf_fit_batch_device(d_img.data_ptr(), W, H, spf, d_ini.data_ptr(), ctypes.byref(ccfg),
+                                         d_out.data_ptr(), d_ab[0].data_ptr(), d_ab[1].data_ptr(),
+                                         d_ab[2].data_ptr(), d_u8[0].data_ptr(), d_u8[1].data_ptr(), None, st))
+        d_out[:, 3:].copy_(d_ab.t())
+        pin_out.copy_(d_out, non_blocking=True)
+        pin_u8.copy_(d_u8, non_blocking=True)
+
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            frame_ops()
+    stream.synchronize()
+    graph = None
+    try:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream, capture_error_mode="thread_local"):
+            frame_ops()
+        graph = g
+    except Exception as e:  # keep measuring without a graph rather than failing the bench
+        sys.stderr.write(f"realtime: graph capture failed ({e}); plain launches\n")
+    lat = []
+    for f in range(frames):
+        t0 = time.perf_counter()
+        pin_in.numpy()[:] = allimg[f]  # the camera frame lands in pinned staging
+        if graph is not None:
+            graph.replay()
+        else:
+            with torch.cuda.stream(stream):
+                frame_ops()
+        stream.synchronize()
+        lat.append(time.perf_counter() - t0)
+    lat_us = np.array(lat) * 1e6
+    return {"spots_per_frame": spf, "frames": frames, "grid": f"{W}x{H}", "cuda_graph": graph is not None,
+            "p50_us": float(np.percentile(lat_us, 50)), "p99_us": float(np.percentile(lat_us, 99)),
+            "max_us": float(lat_us.max()), "mean_us": float(lat_us.mean()),
+            "sustains_1kHz": bool(np.percentile(lat_us, 99) < 1000.0),
+            "span": "host frame copy -> H2D -> GPU initializer -> LM fit -> D2H (blocking per frame)"}
+
+
 def run_ours(args):
     import torch
 
@@ -188,14 +260,26 @@ def run_ours(args):
     from paper_2106_02045_b200 import _lib
 
     rank, world, local = dist_env()
+    ndev = torch.cuda.device_count()
+    torch.cuda.set_device(local % ndev)
+    dev = torch.cuda.current_device()
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(0)
-    dev = torch.cuda.current_device()
+        # plumbing only (barrier + max-over-ranks timing): NCCL with one rank per GPU; gloo when ranks share a
+        # GPU (SPOTFIT_DIST_BACKEND=gloo, used to exercise this path on a single-GPU box)
+        backend = os.environ.get("SPOTFIT_DIST_BACKEND", "nccl" if ndev >= world else "gloo")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group("gloo")
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=dev if torch.distributed.get_backend() == "nccl" else "cpu")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
     W, H, count, model = CONFIGS[args.config]
     if args.count:
         count = args.count
@@ -247,11 +331,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     evs = d_ev.cpu().tolist()
-    ms_max = ms
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms_max = float(t.item())
+    ms_max = max_over_ranks(ms)
     fits = count * world * args.steps
     value = fits / (ms_max * 1e-3)
 
@@ -269,26 +349,24 @@ def run_ours(args):
         (count, torch.uint8), (count, torch.uint8)]])
     engine = "implicit3" if model == 3 else "elliptical"
     for _ in range(max(1, args.warmup)):
-        sf.fit_batch(pin_img.numpy(), pin_ini.numpy(), config=cfg, engine=engine, grid=grid, out=outs)
+        sf.fit_batch(pin_img.numpy(), pin_ini.numpy(), config=cfg, engine=engine, grid=grid, out=outs, devices=[dev])
     barrier()
     e2e_steps = max(3, args.steps // 2)
     chunks = 0
-    t_host = []
-    for _ in range(e2e_steps):
+    e2e_s = 0.0
+    for _ in range(e2e_steps):  # blocking public call: host clock, max over ranks per step
         barrier()
         a = time.perf_counter()
-        r = sf.fit_batch(pin_img.numpy(), pin_ini.numpy(), config=cfg, engine=engine, grid=grid, out=outs)
-        t_host.append(time.perf_counter() - a)
+        r = sf.fit_batch(pin_img.numpy(), pin_ini.numpy(), config=cfg, engine=engine, grid=grid, out=outs,
+                         devices=[dev])
+        e2e_s += max_over_ranks(time.perf_counter() - a)
         chunks = r.stats["n_chunks"]
-    e2e_s = float(np.sum(t_host))
-    if world > 1:
-        t = torch.tensor([e2e_s], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_s = float(t.item())
     e2e_value = count * world * e2e_steps / e2e_s
 
     # ---- parity on a sample (GPU vs C oracle, bitwise) and CPU baselines (rank 0)
     result = {}
+    if rank == 0 and args.rt_frames > 0:
+        result["realtime"] = realtime(args, dev)
     if rank == 0:
         from oracle import lm, oracle_c
 
@@ -390,6 +468,8 @@ def main(argv=None):
     ap.add_argument("--ref-sample", type=int, default=0)
     ap.add_argument("--parity-sample", type=int, default=20000)
     ap.add_argument("--profile", action="store_true", help="kernel leg only (for ncu); prints no bench line")
+    ap.add_argument("--rt-spots", type=int, default=50, help="real-time mode: spots per frame (C5)")
+    ap.add_argument("--rt-frames", type=int, default=1000, help="real-time mode frames (0 disables)")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3
