@@ -150,6 +150,15 @@ typedef struct sf_sim_config {
 int sf_simulate_host(const sf_sim_config* cfg, int32_t width, int32_t height, int64_t first_index, int64_t count,
                      float* images, float* truth, int32_t threads);
 
+/*
+ * sf_simulate_device -- the same generator on the GPU: writes
+ * d_images [count][H][W] and d_truth [count][P+2] (or NULL) in device memory on
+ * `stream`.  Integer draws are identical to sf_simulate_host; pixels match it
+ * except where CUDA's f64 libm and glibc round a .5 boundary differently.
+ */
+int sf_simulate_device(const sf_sim_config* cfg, int32_t width, int32_t height, int64_t first_index, int64_t count,
+                       float* d_images, float* d_truth, void* stream);
+
 /* pinned host allocations (so that callers' buffers DMA directly) */
 void* sf_host_alloc(size_t bytes);
 void sf_host_free(void* p);

@@ -29,7 +29,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off",
                      "-Xptxas", "-v", f"-I{INCLUDE}", f"-I{CSRC}"]
 UNITS = [(p, s) for p in (3, 4) for s in (1, 2, 4, 8, 16)]
-HEADERS = ["sf_device.cuh", "sf_fit_kernel.cuh", "sf_launch.h", "sf_geometry.h"]
+HEADERS = ["sf_device.cuh", "sf_fit_kernel.cuh", "sf_launch.h", "sf_geometry.h", "sf_sim_core.h"]
 
 
 def nvcc() -> str:
@@ -70,13 +70,13 @@ def build(force: bool = False, jobs: int = 0, verbose: bool = False, variant: st
         out = os.path.join(obj, f"sf_inst_P{p}_S{s}.o")
         cmd = [nvcc()] + NVCC_FLAGS + dflags + [f"-DSF_P={p}", f"-DSF_SLOTS={s}", "-c", src, "-o", out]
         tasks.append((out, [src] + hdrs, cmd))
-    for name in ("sf_init.cu", "sf_capi.cu"):
+    for name in ("sf_init.cu", "sf_capi.cu", "sf_sim.cu"):
         src = os.path.join(CSRC, name)
         out = os.path.join(obj, name.replace(".cu", ".o"))
         tasks.append((out, [src] + hdrs, [nvcc()] + NVCC_FLAGS + dflags + ["-c", src, "-o", out]))
     src = os.path.join(CSRC, "sf_sim.cpp")
-    out = os.path.join(obj, "sf_sim.o")
-    tasks.append((out, [src, os.path.join(INCLUDE, "spotfit.h"), __file__],
+    out = os.path.join(obj, "sf_sim_host.o")
+    tasks.append((out, [src, os.path.join(CSRC, "sf_sim_core.h"), os.path.join(INCLUDE, "spotfit.h"), __file__],
                   ["g++", "-O2", "-fPIC", "-std=c++17", "-ffp-contract=off", "-pthread", f"-I{INCLUDE}", "-c", src,
                    "-o", out]))
     todo = [t for t in tasks if force or _stale(t[0], t[1])]

@@ -350,6 +350,18 @@ extern "C" {
 
 int sf_version(void) { return SF_ABI_VERSION; }
 
+int sf_simulate_device(const sf_sim_config* cfg, int32_t width, int32_t height, int64_t first_index, int64_t count,
+                       float* d_images, float* d_truth, void* stream) {
+  if (!cfg) return fail("cfg is NULL");
+  if (check_grid(width, height) != 0) return -1;
+  if (cfg->model != 3 && cfg->model != 4) return fail("model must be 3 or 4");
+  if (count < 0) return fail("negative count");
+  cudaError_t e = sf::launch_simulate(*cfg, width, height, first_index, count, d_images, d_truth,
+                                      static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail("simulator launch failed: %s", cudaGetErrorString(e));
+  return 0;
+}
+
 int sf_debug_npexp_device(const float* d_x, float* d_y, int64_t n, int32_t variant, void* stream) {
   if (n < 0 || (variant != 0 && variant != 1)) return fail("bad arguments");
   cudaError_t e = sf::launch_npexp(d_x, d_y, n, variant, static_cast<cudaStream_t>(stream));

@@ -48,6 +48,10 @@ SF_DECLARE_UNIT(4, 16)
 cudaError_t launch_estimate_initial(const float* images, int W, int H, int64_t count, int P, double sigma_min,
                                     double sigma_max, float* inits, float* amps, cudaStream_t stream);
 
+// device simulator (sf_sim.cu)
+cudaError_t launch_simulate(const sf_sim_config& c, int W, int H, int64_t first, int64_t count, float* images,
+                            float* truth, cudaStream_t stream);
+
 // exhaustive-check helper (sf_init.cu)
 cudaError_t launch_npexp(const float* x, float* y, int64_t n, int variant, cudaStream_t stream);
 

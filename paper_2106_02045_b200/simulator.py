@@ -50,6 +50,22 @@ def simulate_batch(cfg: SimConfig, first_index: int = 0, threads: int = 0):
     return images, truth
 
 
+def simulate_batch_device(cfg: SimConfig, first_index: int = 0, device=None):
+    """The generator on the GPU (sf_simulate_device): -> (images (count, H, W),
+    truth (count, P+2)) as CUDA tensors, generated in HBM (no PCIe)."""
+    import torch
+
+    _lib.require_gpu()
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    images = torch.empty((cfg.count, cfg.height, cfg.width), dtype=torch.float32, device=dev)
+    truth = torch.empty((cfg.count, cfg.model + 2), dtype=torch.float32, device=dev)
+    c = cfg.to_c()
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    _lib.check(_lib.lib().sf_simulate_device(ctypes.byref(c), cfg.width, cfg.height, first_index, cfg.count,
+                                             images.data_ptr(), truth.data_ptr(), stream))
+    return images, truth
+
+
 def simulate_spot(cfg: SimConfig, index: int):
     """One spot by index: equals simulate_batch(...)[index]."""
     one = SimConfig(**{**cfg.__dict__, "count": 1})
