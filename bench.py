@@ -39,12 +39,13 @@ CONFIGS = {
     "c1": (11, 11, 10_000, 3),
     "c3": (21, 21, 1_000_000, 4),
     "c4": (32, 32, 1_000_000, 3),
+    "c2x": (15, 15, 1_000_000, 5),  # explicit 5-parameter baseline on the C2 workload
 }
 METRIC = "2D Gaussian fits/sec (15x15 px) at 1/2/4/8 B200 vs CPU ref; % FP32/SFU roofline"
 # algorithmic work per pixel-evaluation: G-eval 67 ops (45 FP32 + 22 reduction adds),
 # T-eval 18 ops (14 + 4); one exp each.  Elliptical G-eval: 58 + 30.
-OPS_G = {3: 67, 4: 88}
-OPS_T = {3: 18, 4: 18}
+OPS_G = {3: 67, 4: 88, 5: 60}  # explicit-5: 39 FP32 + 21 reduction adds per pixel-evaluation (G = T)
+OPS_T = {3: 18, 4: 18, 5: 60}
 
 
 def dist_env():
@@ -111,7 +112,8 @@ def load_peaks():
 def make_workload(W, H, count, model, seed):
     import paper_2106_02045_b200 as sf
 
-    im, _ = sf.simulate_batch(sf.SimConfig(width=W, height=H, count=count, seed=seed, model=model))
+    sim_model = 4 if model == 4 else 3  # explicit-5 fits symmetric spots
+    im, _ = sf.simulate_batch(sf.SimConfig(width=W, height=H, count=count, seed=seed, model=sim_model))
     return im.reshape(count, W * H)
 
 
@@ -125,7 +127,7 @@ def cpu_reference(W, H, model, images, inits, sample, workers):
     (kind "port")."""
     from oracle import lm
 
-    backend = "auto" if model == 3 else "port"
+    backend = "auto" if model in (3, 5) else "port"
     _, kind = lm.model_backend(backend)
     cfg = lm.LMConfig.for_grid(W, H)
     t0 = time.perf_counter()
@@ -154,7 +156,9 @@ def run_reference(args):
     cores = len(os.sched_getaffinity(0))
     sample = args.ref_sample or max(2000, 500 * cores)
     images = make_workload(W, H, sample, model, seed=2021)
-    inits, _ = oinit.estimate_initial_batch(images, W, H, 0.3, float(max(W, H)), model)
+    inits, amps = oinit.estimate_initial_batch(images, W, H, 0.3, float(max(W, H)), min(model, 4))
+    if model == 5:
+        inits = np.concatenate([inits, amps], axis=1).astype(np.float32)
     for _ in range(args.warmup):
         cpu_reference(W, H, model, images, inits, min(sample, 64 * cores), cores)
     times = []
@@ -293,7 +297,7 @@ def run_ours(args):
     t0 = time.perf_counter()
     images = make_workload(W, H, count, model, seed=1000 + rank)
     d_img = torch.from_numpy(images).to(dev)
-    d_ini = sf.batch_engine.estimate_initial_device(d_img, grid, model, cfg)
+    d_ini = sf.batch_engine._auto_inits(d_img, grid, model, cfg)
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t0
     d_par = torch.empty((count, model), dtype=torch.float32, device=dev)
@@ -347,7 +351,7 @@ def run_ours(args):
     outs = sf.BatchResult(*[torch.empty(s, dtype=d).pin_memory().numpy() for s, d in [
         ((count, model), torch.float32), (count, torch.float32), (count, torch.float32), (count, torch.float32),
         (count, torch.uint8), (count, torch.uint8)]])
-    engine = "implicit3" if model == 3 else "elliptical"
+    engine = {3: "implicit3", 4: "elliptical", 5: "explicit5"}[model]
     for _ in range(max(1, args.warmup)):
         sf.fit_batch(pin_img.numpy(), pin_ini.numpy(), config=cfg, engine=engine, grid=grid, out=outs, devices=[dev])
     barrier()
@@ -411,7 +415,7 @@ def run_ours(args):
     sfu_peak = sms * 16 * sm_max * 1e6
     achieved = ops / launch_s
     hbm_bytes = count * (4 * N + 4 * model) + count * (4 * model + 12 + 2)
-    f2f_per_pix = {3: 22, 4: 30}[model]
+    f2f_per_pix = {3: 22, 4: 30, 5: 21}[model]
     f2f_ops = N * n_k * f2f_per_pix
     if rank == 0:
         line = {

@@ -46,6 +46,9 @@ extern "C" {
 /* model selector */
 #define SF_MODEL_SYMMETRIC 3  /* (x, y, sigma)            model.py:100-115 */
 #define SF_MODEL_ELLIPTICAL 4 /* (x, y, sigma_x, sigma_y) SURVEY App. B.5, no reference */
+/* explicit 5-parameter baseline fit_explicit5: LM over (x, y, sigma, alpha,
+ * beta), 5x5 pivoted solve, sigma free in sign; inits and out_params are [count][5] */
+#define SF_MODEL_EXPLICIT5 5
 
 /* FitConfig + ParameterBounds (defaults) */
 typedef struct sf_config {

@@ -56,10 +56,60 @@ def _clamp(v: float, lo: float, hi: float) -> float:
 
 
 def limit(v, W: int, H: int, c: LMConfig) -> list:
-    """clamp in f64, then quantise to f32 once (App. A [A4])."""
+    """clamp in f64, then quantise to f32 once (App. A [A4]).
+    Explicit-5 (len 5): sigma free in sign with |sigma| bounded, alpha/beta free."""
     out = [_clamp(v[0], -c.margin_x, (W - 1) + c.margin_x), _clamp(v[1], -c.margin_y, (H - 1) + c.margin_y)]
-    out += [_clamp(s, c.sigma_min, c.sigma_max) for s in v[2:]]
+    if len(v) == 5:
+        s = v[2]
+        out += [-_clamp(-s, c.sigma_min, c.sigma_max) if s < 0 else _clamp(s, c.sigma_min, c.sigma_max), v[3], v[4]]
+    else:
+        out += [_clamp(s, c.sigma_min, c.sigma_max) for s in v[2:]]
     return [float(np.float32(t)) for t in out]
+
+
+def solve_pivot5(jtj_packed, rhs, lam: float):
+    """Explicit-5 step: damped 5x5 system by Gaussian elimination
+    with partial pivoting, f64, no FMA; None on StepFailed (zero pivot or
+    |det| <= 1e-12 * prod(damped diagonal)).  Twin of spotfit_oracle.c:solve_pivot5."""
+    P = 5
+    M = [[0.0] * P for _ in range(P)]
+    m = 0
+    for i in range(P):
+        for j in range(i, P):
+            M[i][j] = M[j][i] = float(jtj_packed[m])
+            m += 1
+    b = [float(x) for x in rhs]
+    for i in range(P):
+        M[i][i] = M[i][i] + lam * M[i][i]
+    dprod = M[0][0]
+    for i in range(1, P):
+        dprod = dprod * M[i][i]
+    det = 1.0
+    for col in range(P):
+        pr, best = col, abs(M[col][col])
+        for r in range(col + 1, P):
+            if abs(M[r][col]) > best:
+                best, pr = abs(M[r][col]), r
+        if not (best > 0.0):
+            return None
+        if pr != col:
+            M[col], M[pr] = M[pr], M[col]
+            b[col], b[pr] = b[pr], b[col]
+        det = det * M[col][col]
+        for r in range(col + 1, P):
+            fct = M[r][col] / M[col][col]
+            for c in range(col, P):
+                M[r][c] = M[r][c] - fct * M[col][c]
+            b[r] = b[r] - fct * b[col]
+    if not (abs(det) > STEP_GUARD * abs(dprod)):
+        return None
+    delta = [0.0] * P
+    for r in reversed(range(P)):
+        s = b[r]
+        for c in range(r + 1, P):
+            s = s - M[r][c] * delta[c]
+        delta[r] = s / M[r][r]
+    return delta
 
 
 def solve_step(jtj_packed, rhs, lam: float):
@@ -69,6 +119,8 @@ def solve_step(jtj_packed, rhs, lam: float):
     CUDA kernel).  Returns None on StepFailed: a non-positive pivot or
     det <= 1e-12 * prod(damped diagonal)."""
     P = len(rhs)
+    if P == 5:
+        return solve_pivot5(jtj_packed, rhs, lam)
     A = [[0.0] * P for _ in range(P)]
     m = 0
     for i in range(P):
@@ -125,8 +177,28 @@ def _params(m, p):
     return m.ShapeParams(*p)
 
 
+def explicit5_eval(m, image, p) -> _Eval:
+    """Explicit 5-parameter model, p = (x, y, sigma, alpha, beta):
+    h = alpha*f + beta, d = (alpha*df/dx, alpha*df/dy, alpha*df/dsigma, f, 1) in f32,
+    chi^2 / rhs / JtJ as f64 numpy-order sums of f32 products."""
+    e = _Eval()
+    f, fg = m.profile_and_gradient(m.ShapeParams(*p[:3]), image.grid)
+    a32, b32 = np.float32(p[3]), np.float32(p[4])
+    g = image.values
+    r = g - (a32 * f + b32)
+    d = [a32 * fg[:, 0], a32 * fg[:, 1], a32 * fg[:, 2], f, np.ones_like(f)]
+    e.singular = False
+    e.chi = float(np.float32((r * r).sum(dtype=np.float64)))
+    e.alpha, e.beta = float(a32), float(b32)
+    e.rhs = [float((r * dj).sum(dtype=np.float64)) for dj in d]
+    e.jtj = [float((d[j] * d[k]).sum(dtype=np.float64)) for j in range(5) for k in range(j, 5)]
+    return e
+
+
 def g_eval(m, image, p) -> _Eval:
     """PAPER.md:139 Gaussian2D(..., gradient=true): chi^2, JtJ and rhs = Jt r."""
+    if len(p) == 5:
+        return explicit5_eval(m, image, p)
     e = _Eval()
     f, fg = m.profile_and_gradient(_params(m, p), image.grid)
     try:
@@ -148,6 +220,8 @@ def g_eval(m, image, p) -> _Eval:
 
 def t_eval(m, image, p) -> _Eval:
     """PAPER.md:151 Gaussian2D(..., gradient=false): profile -> alpha_beta -> chi^2."""
+    if len(p) == 5:
+        return explicit5_eval(m, image, p)
     e = _Eval()
     f = m.profile(_params(m, p), image.grid)
     try:

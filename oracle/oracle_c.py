@@ -56,8 +56,8 @@ class OracleEval(ctypes.Structure):
         ("gamma", ctypes.c_double * 4),
         ("dalpha", ctypes.c_double * 4),
         ("dbeta", ctypes.c_double * 4),
-        ("rhs", ctypes.c_double * 4),
-        ("jtj", ctypes.c_double * 10),
+        ("rhs", ctypes.c_double * 5),
+        ("jtj", ctypes.c_double * 15),
     ]
 
 
@@ -78,8 +78,8 @@ EVAL_DTYPE = np.dtype(
         ("gamma", np.float64, 4),
         ("dalpha", np.float64, 4),
         ("dbeta", np.float64, 4),
-        ("rhs", np.float64, 4),
-        ("jtj", np.float64, 10),
+        ("rhs", np.float64, 5),
+        ("jtj", np.float64, 15),
     ],
     align=True,
 )

@@ -131,12 +131,50 @@ double pw_sum(const float* a, int n) { return 0.0 + pw_rec(a, n); }
 /* ------------------------------------------------------------------ */
 #define DENOM_GUARD 1e-12 /* model.py:28 */
 
+/* Explicit 5-parameter model (the Gpufit-like baseline; no
+ * reference code -- pinned here in the same numeric style): p = (x, y, sigma,
+ * alpha, beta), h = alpha*f + beta, model derivatives
+ * d = (alpha*df/dx, alpha*df/dy, alpha*df/dsigma, f, 1) in f32, chi^2, rhs = sum r*d
+ * and JtJ = sum d_j*d_k as f64 numpy-order sums of f32 products. */
+static int eval_explicit5(const float* g, int W, int H, const float* p, sf_oracle_eval_t* e) {
+  const int N = W * H;
+  float t[SF_ORACLE_MAXPIX], d[5][SF_ORACLE_MAXPIX], r[SF_ORACLE_MAXPIX];
+  const float x0 = p[0], y0 = p[1], inv = 1.0f / p[2], a32 = p[3], b32 = p[4];
+  for (int i = 0; i < N; ++i) {
+    const float xi = (float)(i % W), yi = (float)(i / W);
+    const float u = (xi - x0) * inv, v = (yi - y0) * inv;
+    const float uu = u * u, vv = v * v;
+    const float q = uu + vv;
+    const float f = npexp_f32(-0.5f * q);
+    const float fs = f * inv;
+    const float f0 = u * fs, f1 = v * fs, f2 = q * fs;
+    const float h = a32 * f + b32;
+    r[i] = g[i] - h;
+    d[0][i] = a32 * f0; d[1][i] = a32 * f1; d[2][i] = a32 * f2; d[3][i] = f; d[4][i] = 1.0f;
+  }
+  for (int i = 0; i < N; ++i) t[i] = r[i] * r[i];
+  e->chi = (float)pw_sum(t, N);
+  e->alpha = a32; e->beta = b32;
+  for (int j = 0; j < 5; ++j) {
+    for (int i = 0; i < N; ++i) t[i] = r[i] * d[j][i];
+    e->rhs[j] = pw_sum(t, N);
+  }
+  int m = 0;
+  for (int j = 0; j < 5; ++j)
+    for (int k = j; k < 5; ++k) {
+      for (int i = 0; i < N; ++i) t[i] = d[j][i] * d[k][i];
+      e->jtj[m++] = pw_sum(t, N);
+    }
+  return 0;
+}
+
 int sf_oracle_eval(const float* g, int W, int H, int P, const float* p, sf_oracle_eval_t* e) {
   const int N = W * H;
   float f[SF_ORACLE_MAXPIX], fg[4][SF_ORACLE_MAXPIX], t[SF_ORACLE_MAXPIX];
   float d[4][SF_ORACLE_MAXPIX], r[SF_ORACLE_MAXPIX];
   memset(e, 0, sizeof(*e));
-  if (N < 1 || N > SF_ORACLE_MAXPIX || (P != 3 && P != 4)) return -1;
+  if (N < 1 || N > SF_ORACLE_MAXPIX || P < 3 || P > 5) return -1;
+  if (P == 5) return eval_explicit5(g, W, H, p, e);
   /* _scaled_offsets (model.py:154-165) / profile_and_gradient (model.py:180-199) */
   if (P == 3) {
     const float x0 = p[0], y0 = p[1], inv = 1.0f / p[2];
@@ -221,7 +259,48 @@ static inline int sym_idx(int P, int i, int j) { /* upper-packed row-major */
   return i * P - (i * (i - 1)) / 2 + (j - i);
 }
 
+/* explicit-5 step ("a 5x5 damped system solved by elimination with
+ * partial pivoting"): f64, no FMA, first maximal |pivot| on ties; StepFailed on a
+ * zero pivot or |det| <= 1e-12 * prod(damped diagonal). */
+static int solve_pivot5(const double* jtj, const double* rhs, double lam, double* delta) {
+  enum { P = 5 };
+  double M[P][P], b[P];
+  for (int i = 0; i < P; ++i) {
+    for (int j = 0; j < P; ++j) M[i][j] = jtj[sym_idx(P, i, j)];
+    b[i] = rhs[i];
+  }
+  for (int i = 0; i < P; ++i) M[i][i] = M[i][i] + lam * M[i][i];
+  double dprod = M[0][0];
+  for (int i = 1; i < P; ++i) dprod = dprod * M[i][i];
+  double det = 1.0;
+  for (int col = 0; col < P; ++col) {
+    int pr = col;
+    double best = fabs(M[col][col]);
+    for (int r = col + 1; r < P; ++r)
+      if (fabs(M[r][col]) > best) { best = fabs(M[r][col]); pr = r; }
+    if (!(best > 0.0)) return 0;
+    if (pr != col) {
+      for (int c = 0; c < P; ++c) { double t = M[col][c]; M[col][c] = M[pr][c]; M[pr][c] = t; }
+      double t = b[col]; b[col] = b[pr]; b[pr] = t;
+    }
+    det = det * M[col][col];
+    for (int r = col + 1; r < P; ++r) {
+      const double fct = M[r][col] / M[col][col];
+      for (int c = col; c < P; ++c) M[r][c] = M[r][c] - fct * M[col][c];
+      b[r] = b[r] - fct * b[col];
+    }
+  }
+  if (!(fabs(det) > SF_STEP_GUARD * fabs(dprod))) return 0;
+  for (int r = P - 1; r >= 0; --r) {
+    double s = b[r];
+    for (int c = r + 1; c < P; ++c) s = s - M[r][c] * delta[c];
+    delta[r] = s / M[r][r];
+  }
+  return 1;
+}
+
 int sf_oracle_solve(int P, const double* jtj, const double* rhs, double lam, double* delta) {
+  if (P == 5) return solve_pivot5(jtj, rhs, lam, delta);
   double A[4][4], L[4][4], C[4][4], D[4], z[4];
   for (int i = 0; i < P; ++i)
     for (int j = 0; j < P; ++j) A[i][j] = jtj[sym_idx(P, i, j)];
@@ -265,6 +344,12 @@ static inline double clampd(double v, double lo, double hi) {
 static void limit_params(int P, int W, int H, const sf_oracle_config_t* c, const double* v, float* out) {
   out[0] = (float)clampd(v[0], -c->margin_x, (double)(W - 1) + c->margin_x);
   out[1] = (float)clampd(v[1], -c->margin_y, (double)(H - 1) + c->margin_y);
+  if (P == 5) {  /* explicit-5: sigma free in sign, |sigma| bounded; alpha, beta free */
+    out[2] = (float)(v[2] < 0.0 ? -clampd(-v[2], c->sigma_min, c->sigma_max) : clampd(v[2], c->sigma_min, c->sigma_max));
+    out[3] = (float)v[3];
+    out[4] = (float)v[4];
+    return;
+  }
   for (int j = 2; j < P; ++j) out[j] = (float)clampd(v[j], c->sigma_min, c->sigma_max);
 }
 
@@ -282,7 +367,7 @@ int sf_oracle_fit(const float* g, int W, int H, int P, const float* init, const 
                   sf_oracle_result_t* res) {
   const int N = W * H;
   memset(res, 0, sizeof(*res));
-  if (N < 1 || N > SF_ORACLE_MAXPIX || (P != 3 && P != 4)) return -1;
+  if (N < 1 || N > SF_ORACLE_MAXPIX || P < 3 || P > 5) return -1;
   /* InvalidInput: per-image status, not a batch failure */
   int bad = 0;
   for (int i = 0; i < N; ++i) bad |= !isfinite(g[i]);
@@ -294,8 +379,8 @@ int sf_oracle_fit(const float* g, int W, int H, int P, const float* init, const 
     res->iterations = 0;
     return 0;
   }
-  float p[4], best[4], trial[4];
-  double v[4], delta[4], thr[4];
+  float p[5], best[5], trial[5];
+  double v[5], delta[5], thr[5];
   sf_oracle_eval_t Eb, Et;
   {
     for (int j = 0; j < P; ++j) v[j] = (double)init[j];
@@ -409,7 +494,7 @@ int sf_oracle_fit_batch(const float* images, int W, int H, int64_t count, int P,
                         const sf_oracle_config_t* c, float* out_params, float* out_alpha, float* out_beta,
                         float* out_nchi2, uint8_t* out_status, uint8_t* out_iters, int threads) {
   const int N = W * H;
-  if (N < 1 || N > SF_ORACLE_MAXPIX || (P != 3 && P != 4) || c->max_iterations < 1 || c->max_iterations > 255)
+  if (N < 1 || N > SF_ORACLE_MAXPIX || P < 3 || P > 5 || c->max_iterations < 1 || c->max_iterations > 255)
     return -1;
   sf_chunk_t k;
   memset(&k, 0, sizeof(k));

@@ -31,12 +31,12 @@ typedef struct {
   float alpha, beta, chi;
   double F, G, FF, FG, denom;
   double dF[4], dFF[4], dFG[4], gamma[4], dalpha[4], dbeta[4];
-  double rhs[4];
-  double jtj[10];
+  double rhs[5];   /* P = 5: explicit (x, y, sigma, alpha, beta) model */
+  double jtj[15];
 } sf_oracle_eval_t;
 
 typedef struct {
-  float params[4];
+  float params[5];
   float alpha, beta, nchi2;
   uint8_t status, iterations;
 } sf_oracle_result_t;

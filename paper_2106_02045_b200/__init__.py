@@ -9,12 +9,13 @@ from .model import (MAX_PIXELS, DENOM_GUARD, Amplitudes, EllipticalParams, Gradi
                     PixelGrid, ProfileSums, ShapeParams, SingularProfile, SpotImage, evaluate, evaluate_batch)
 from .solver import FitConfig, FitResult, ParameterBounds, StopReason, fit_single
 from .batch_engine import BatchRequest, BatchResult, fit_batch
-from .simulator import SimConfig, simulate_batch, simulate_spot
+from .simulator import SimConfig, simulate_batch, simulate_batch_device, simulate_spot
 from .initializer import estimate_initial, estimate_initial_batch
 
 __all__ = [
     "MAX_PIXELS", "DENOM_GUARD", "Amplitudes", "EllipticalParams", "GradientSums", "ModelEvaluation", "PixelGrid",
     "ProfileSums", "ShapeParams", "SingularProfile", "SpotImage", "evaluate", "evaluate_batch", "FitConfig",
     "FitResult", "ParameterBounds", "StopReason", "fit_single", "BatchRequest", "BatchResult", "fit_batch",
-    "SimConfig", "simulate_batch", "simulate_spot", "estimate_initial", "estimate_initial_batch",
+    "SimConfig", "simulate_batch", "simulate_batch_device", "simulate_spot", "estimate_initial",
+    "estimate_initial_batch",
 ]

@@ -19,7 +19,19 @@ from . import _lib
 from .model import PixelGrid, SpotImage, params_array
 from .solver import FitConfig, FitResult, StopReason
 
-ENGINES = {"implicit3": 3, "symmetric": 3, "implicit4": 4, "elliptical": 4}
+# engine -> LM parameter count; explicit5 is the SPEC.md:229-235 comparison baseline
+# (x, y, sigma, alpha, beta with a 5x5 pivoted solve; inits and params are (count, 5))
+ENGINES = {"implicit3": 3, "symmetric": 3, "implicit4": 4, "elliptical": 4, "explicit5": 5}
+
+
+def _auto_inits(images_cuda, grid, P, config):
+    """GPU initializer; explicit5 also takes the initial alpha, beta."""
+    if P == 5:
+        import torch
+
+        ini, am = estimate_initial_device(images_cuda, grid, 3, config, amps=True)
+        return torch.cat([ini, am], dim=1).contiguous()
+    return estimate_initial_device(images_cuda, grid, P, config)
 
 
 @dataclass
@@ -111,8 +123,6 @@ def fit_batch(images, inits=None, config: FitConfig = FitConfig(), engine: str =
         r = images
         return fit_batch(r.images, r.inits, r.config, r.engine, r.devices, r.grid, out)
     if engine not in ENGINES:
-        if engine == "explicit5":
-            raise NotImplementedError("explicit5 (SPEC.md:229-235) is a comparison baseline outside this build")
         raise ValueError(f"unknown engine {engine!r}")
     P = ENGINES[engine]
     imgs, grid = _as_image_array(images, grid)
@@ -127,7 +137,7 @@ def fit_batch(images, inits=None, config: FitConfig = FitConfig(), engine: str =
 
         dev = imgs.device
         if inits is None:
-            ini = estimate_initial_device(imgs, grid, P, config)
+            ini = _auto_inits(imgs, grid, P, config)
         else:
             ini = torch.as_tensor(params_array(inits) if not isinstance(inits, torch.Tensor) else inits,
                                   dtype=torch.float32, device=dev).reshape(count, P).contiguous()
@@ -148,7 +158,7 @@ def fit_batch(images, inits=None, config: FitConfig = FitConfig(), engine: str =
     if inits is None:
         import torch
 
-        ini = estimate_initial_device(torch.as_tensor(imgs).cuda(), grid, P, config).cpu().numpy()
+        ini = _auto_inits(torch.as_tensor(imgs).cuda(), grid, P, config).cpu().numpy()
     else:
         ini = np.ascontiguousarray(params_array(inits), dtype=np.float32).reshape(count, P)
     if out is None:

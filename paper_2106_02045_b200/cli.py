@@ -89,20 +89,28 @@ def cmd_fit(a):
     from .io_formats import read_truth_csv, write_params_csv
     from .model import PixelGrid
 
-    if a.engine not in ("implicit3", "elliptical"):
-        raise CliError(EXIT_ARGS, f"engine {a.engine!r} is not available in this build (implicit3 | elliptical)")
+    engines = {"implicit3": 3, "elliptical": 4, "explicit5": 5}
+    if a.engine not in engines:
+        raise CliError(EXIT_ARGS, f"unknown engine {a.engine!r} (implicit3 | explicit5 | elliptical)")
     images, W, H = _load_spb1(a.inp)
     cfg = _fit_config(a)
-    P = 3 if a.engine == "implicit3" else 4
+    P = engines[a.engine]
     grid = PixelGrid(W, H)
     count = images.shape[0]
     flat = np.ascontiguousarray(images).reshape(count, W * H)
     t0 = time.perf_counter()
     if a.inits in (None, "auto"):
-        inits = estimate_initial_batch(flat, P, cfg, grid=grid)[0] if count else np.zeros((0, P), np.float32)
+        if count == 0:
+            inits = np.zeros((0, P), np.float32)
+        elif P == 5:  # explicit5 also starts from the initializer's alpha, beta
+            ini, amps = estimate_initial_batch(flat, 3, cfg, grid=grid)
+            inits = np.concatenate([ini, amps], axis=1)
+        else:
+            inits = estimate_initial_batch(flat, P, cfg, grid=grid)[0]
     else:
         try:
-            inits = read_truth_csv(a.inits)[:, :P]
+            t = read_truth_csv(a.inits)  # x, y, sigma[, sigma_y], alpha, beta
+            inits = np.concatenate([t[:, :3], t[:, -2:]], axis=1) if P == 5 else t[:, :P]
         except (OSError, ValueError) as e:
             raise CliError(EXIT_IO, f"cannot read inits {a.inits}: {e}")
         if len(inits) != count:

@@ -46,7 +46,8 @@ int check_grid(int W, int H) {
 
 int make_cfg(const sf_config* c, int W, int H, sf::Cfg& k) {
   if (c == nullptr) return fail("cfg is NULL");
-  if (c->model != SF_MODEL_SYMMETRIC && c->model != SF_MODEL_ELLIPTICAL) return fail("model must be 3 or 4");
+  if (c->model != SF_MODEL_SYMMETRIC && c->model != SF_MODEL_ELLIPTICAL && c->model != SF_MODEL_EXPLICIT5)
+    return fail("model must be 3, 4 or 5");
   if (c->max_iterations < 1 || c->max_iterations > 255) return fail("max_iterations must be in [1, 255]");
   if (!(c->min_delta > 0) || !(c->min_step > 0)) return fail("min_delta and min_step must be > 0");
   if (!(c->max_error >= 0)) return fail("max_error must be >= 0");
@@ -69,8 +70,12 @@ int make_cfg(const sf_config* c, int W, int H, sf::Cfg& k) {
   k.hi[1] = (double)(H - 1) + c->margin_y;
   k.lo[2] = k.lo[3] = c->sigma_min;
   k.hi[2] = k.hi[3] = c->sigma_max;
+  k.lo[4] = -INFINITY;  // explicit-5 beta (free); alpha uses [3] only in the explicit limit (free too)
+  k.hi[4] = INFINITY;
   return 0;
 }
+
+constexpr int kMaxP = 5;  // widest parameter vector (explicit-5) -- staging layout
 
 int sm_count_of_current() {
   int dev = 0, sms = 0;
@@ -96,6 +101,7 @@ int dispatch_fit(int P, const sf::LaunchFit& a) {
   if (P == PP && slots == S) used = sf::launch_fit_P##PP##_S##S(a, &err);
   SF_CASE(3, 1) SF_CASE(3, 2) SF_CASE(3, 4) SF_CASE(3, 8) SF_CASE(3, 16)
   SF_CASE(4, 1) SF_CASE(4, 2) SF_CASE(4, 4) SF_CASE(4, 8) SF_CASE(4, 16)
+  SF_CASE(5, 1) SF_CASE(5, 2) SF_CASE(5, 4) SF_CASE(5, 8) SF_CASE(5, 16)
 #undef SF_CASE
   if (used < 0) return fail("no kernel instantiation for P=%d slots=%d chain=%d tail=%d", P, slots, ch, tl);
   if (err != cudaSuccess) return fail("fit kernel launch failed: %s", cudaGetErrorString(err));
@@ -182,16 +188,16 @@ int ensure_ctx(DevCtx& c, int dev, size_t spots, int npix, int P, bool staging) 
     if (!grow) continue;
     free_slot_buffers(s);
     SF_CUDA(cudaMalloc(&s.d_img, spots * npix * sizeof(float)));
-    SF_CUDA(cudaMalloc(&s.d_init, spots * 4 * sizeof(float)));
-    SF_CUDA(cudaMalloc(&s.d_par, spots * 4 * sizeof(float)));
+    SF_CUDA(cudaMalloc(&s.d_init, spots * kMaxP * sizeof(float)));
+    SF_CUDA(cudaMalloc(&s.d_par, spots * kMaxP * sizeof(float)));
     SF_CUDA(cudaMalloc(&s.d_a, spots * sizeof(float)));
     SF_CUDA(cudaMalloc(&s.d_b, spots * sizeof(float)));
     SF_CUDA(cudaMalloc(&s.d_c, spots * sizeof(float)));
     SF_CUDA(cudaMalloc(&s.d_st, spots));
     SF_CUDA(cudaMalloc(&s.d_it, spots));
-    if (staging) {
-      SF_CUDA(cudaHostAlloc(&s.h_in, spots * (npix + 4) * sizeof(float), cudaHostAllocPortable));
-      SF_CUDA(cudaHostAlloc(&s.h_out, spots * (4 + 3 + 1) * sizeof(float), cudaHostAllocPortable));
+    if (staging) {  // h_in: images | inits[kMaxP];  h_out: params[kMaxP] | alpha | beta | nchi2 | status, iters
+      SF_CUDA(cudaHostAlloc(&s.h_in, spots * (npix + kMaxP) * sizeof(float), cudaHostAllocPortable));
+      SF_CUDA(cudaHostAlloc(&s.h_out, spots * (kMaxP + 3 + 1) * sizeof(float), cudaHostAllocPortable));
     }
     s.cap_spots = spots;
     s.cap_npix = npix;
@@ -246,10 +252,10 @@ void copy_out_staged(Slot& s, HostJob& j) {
   const float* o = s.h_out;
   const size_t cap = s.cap_spots;
   std::memcpy(j.par + lo * P, o, n * P * sizeof(float));
-  std::memcpy(j.alpha + lo, o + cap * 4, n * sizeof(float));
-  std::memcpy(j.beta + lo, o + cap * 5, n * sizeof(float));
-  std::memcpy(j.nchi2 + lo, o + cap * 6, n * sizeof(float));
-  const uint8_t* b = reinterpret_cast<const uint8_t*>(o + cap * 7);
+  std::memcpy(j.alpha + lo, o + cap * kMaxP, n * sizeof(float));
+  std::memcpy(j.beta + lo, o + cap * (kMaxP + 1), n * sizeof(float));
+  std::memcpy(j.nchi2 + lo, o + cap * (kMaxP + 2), n * sizeof(float));
+  const uint8_t* b = reinterpret_cast<const uint8_t*>(o + cap * (kMaxP + 3));
   std::memcpy(j.status + lo, b, n);
   std::memcpy(j.iters + lo, b + cap, n);
   s.pending = false;
@@ -317,11 +323,11 @@ int run_shard(int dev, HostJob& j) {
     } else {
       float* o = s.h_out;
       const size_t cap = s.cap_spots;
-      uint8_t* b = reinterpret_cast<uint8_t*>(o + cap * 7);
+      uint8_t* b = reinterpret_cast<uint8_t*>(o + cap * (kMaxP + 3));
       SF_CUDA(cudaMemcpyAsync(o, s.d_par, n * P * sizeof(float), cudaMemcpyDeviceToHost, s.stream));
-      SF_CUDA(cudaMemcpyAsync(o + cap * 4, s.d_a, n * sizeof(float), cudaMemcpyDeviceToHost, s.stream));
-      SF_CUDA(cudaMemcpyAsync(o + cap * 5, s.d_b, n * sizeof(float), cudaMemcpyDeviceToHost, s.stream));
-      SF_CUDA(cudaMemcpyAsync(o + cap * 6, s.d_c, n * sizeof(float), cudaMemcpyDeviceToHost, s.stream));
+      SF_CUDA(cudaMemcpyAsync(o + cap * kMaxP, s.d_a, n * sizeof(float), cudaMemcpyDeviceToHost, s.stream));
+      SF_CUDA(cudaMemcpyAsync(o + cap * (kMaxP + 1), s.d_b, n * sizeof(float), cudaMemcpyDeviceToHost, s.stream));
+      SF_CUDA(cudaMemcpyAsync(o + cap * (kMaxP + 2), s.d_c, n * sizeof(float), cudaMemcpyDeviceToHost, s.stream));
       SF_CUDA(cudaMemcpyAsync(b, s.d_st, n, cudaMemcpyDeviceToHost, s.stream));
       SF_CUDA(cudaMemcpyAsync(b + cap, s.d_it, n, cudaMemcpyDeviceToHost, s.stream));
       s.pending = true;

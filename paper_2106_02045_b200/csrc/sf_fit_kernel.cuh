@@ -108,7 +108,13 @@ __device__ __forceinline__ bool lm_step(LMState<P>& s, const Eval<P>& E, const C
       for (int m = 0; m < T; ++m) jtj[m] = s.sys[m];
 #pragma unroll
       for (int k = 0; k < P; ++k) rhs[k] = s.sys[T + k];
-      if (solve_step<P>(jtj, rhs, s.lam, delta)) {
+      bool solved;
+      if constexpr (P == 5) {
+        solved = solve_pivot5(jtj, rhs, s.lam, delta);
+      } else {
+        solved = solve_step<P>(jtj, rhs, s.lam, delta);
+      }
+      if (solved) {
         double v[P];
         small = true;
 #pragma unroll
@@ -224,7 +230,8 @@ struct LaneSetup {
 };
 
 template <int P, int SLOTS>
-__global__ void __launch_bounds__(threads_per_block<SLOTS>(), SLOTS >= 8 ? 1 : (P == 4 ? SF_MINB_P4 : SF_MINB_P3))
+__global__ void __launch_bounds__(threads_per_block<SLOTS>(),
+                                  SLOTS >= 8 ? 1 : (P == 3 ? SF_MINB_P3 : (P == 4 ? SF_MINB_P4 : 2)))
     fit_kernel(const float* __restrict__ images, const float* __restrict__ inits, int64_t count, const Geom geom,
                const Cfg cfg, FitOut out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -326,7 +333,11 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(), SLOTS >= 8 ? 1 : (
     if (__all_sync(kFull, exhausted)) break;
 
     Eval<P> E;
-    evaluate<P, SLOTS>(S, L.gl, L.own, L.ch, L.tl, G, n, s.p, E);
+    if constexpr (P == 5) {
+      evaluate_explicit5<SLOTS>(S, L.gl, L.own, L.ch, L.tl, s.p, E);
+    } else {
+      evaluate<P, SLOTS>(S, L.gl, L.own, L.ch, L.tl, G, n, s.p, E);
+    }
     if (!exhausted && !skip) {
       n_e += 1;
       if (lm_step<P>(s, E, cfg, out, spot, leader, N, n_g, n_t)) need = true;

@@ -33,6 +33,7 @@ int SF_UNIT_NAME(launch_fit, SF_P, SF_SLOTS)(const LaunchFit& a, cudaError_t* er
   return (int)blocks;
 }
 
+#if SF_P != 5  // model-level evaluation exists for the implicit models only
 int SF_UNIT_NAME(launch_eval, SF_P, SF_SLOTS)(const LaunchEval& a, cudaError_t* err) {
   auto kern = eval_kernel<SF_P, SF_SLOTS>;
   constexpr int tpb = threads_per_block<SF_SLOTS>();
@@ -46,5 +47,6 @@ int SF_UNIT_NAME(launch_eval, SF_P, SF_SLOTS)(const LaunchEval& a, cudaError_t* 
   *err = cudaGetLastError();
   return (int)blocks;
 }
+#endif
 
 }  // namespace sf

@@ -43,6 +43,12 @@ SF_DECLARE_UNIT(4, 4)
 SF_DECLARE_UNIT(4, 8)
 SF_DECLARE_UNIT(4, 16)
 #undef SF_DECLARE_UNIT
+// explicit 5-parameter model (fit only)
+int launch_fit_P5_S1(const LaunchFit& a, cudaError_t* err);
+int launch_fit_P5_S2(const LaunchFit& a, cudaError_t* err);
+int launch_fit_P5_S4(const LaunchFit& a, cudaError_t* err);
+int launch_fit_P5_S8(const LaunchFit& a, cudaError_t* err);
+int launch_fit_P5_S16(const LaunchFit& a, cudaError_t* err);
 
 // initializer kernel launcher (sf_init.cu)
 cudaError_t launch_estimate_initial(const float* images, int W, int H, int64_t count, int P, double sigma_min,

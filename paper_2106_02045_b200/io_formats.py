@@ -86,7 +86,9 @@ def status_name(status: int) -> str:
 
 def write_params_csv(path_or_file, result, first_index: int = 0) -> None:
     """ParamsCSV from a BatchResult-like object (params, alpha, beta, nchi2, status, iterations)."""
-    P = result.params.shape[1]
+    P = min(result.params.shape[1], 4)  # explicit5 rows: (x, y, sigma) + alpha/beta columns
+    if result.params.shape[1] == 5:
+        P = 3
     cols = ["index", "x", "y", "sigma"] + (["sigma_y"] if P == 4 else []) + ["alpha", "beta", "status",
                                                                            "iterations", "nchi2"]
     n = len(result.alpha)

@@ -95,7 +95,8 @@ class FitResult:
     @staticmethod
     def from_row(params, alpha, beta, nchi2, status, iters) -> "FitResult":
         p = [float(v) for v in params]
-        shape = ShapeParams(*p) if len(p) == 3 else EllipticalParams(*p)
+        # explicit5 rows carry (x, y, sigma, alpha, beta); alpha/beta also arrive separately
+        shape = ShapeParams(*p[:3]) if len(p) in (3, 5) else EllipticalParams(*p)
         s = int(status)
         return FitResult(shape, Amplitudes(float(alpha), float(beta)), StopReason(s & 7), int(iters), float(nchi2),
                          bool(s & _lib.SF_FLAG_NOIMP), bool(s & _lib.SF_FLAG_INVALID), s)

@@ -108,7 +108,7 @@ def test_cli_fit_malformed_and_engine(tmp_path):
     open(p, "wb").write(b"NOPE" + b"\x00" * 20)
     assert main(["fit", "--in", str(p), "--out", str(tmp_path / "o.csv")]) == 4
     assert main(["fit", "--in", str(tmp_path / "missing.spb"), "--out", str(tmp_path / "o.csv")]) == 3
-    assert main(["fit", "--in", str(p), "--out", str(tmp_path / "o.csv"), "--engine", "explicit5"]) == 2
+    assert main(["fit", "--in", str(p), "--out", str(tmp_path / "o.csv"), "--engine", "bogus"]) == 2
 
 
 @pytest.mark.gpu
