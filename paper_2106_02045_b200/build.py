@@ -17,7 +17,7 @@ import sys
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
-CSRC = os.path.join(PKG, "csrc")
+CSRC = os.environ.get("SPOTFIT_CSRC") or os.path.join(PKG, "csrc")  # alternate tree for A/B builds
 INCLUDE = os.path.join(ROOT, "include")
 OBJ = os.path.join(PKG, "_build")
 LIBDIR = os.path.join(PKG, "_lib")

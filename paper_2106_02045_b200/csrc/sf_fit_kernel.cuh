@@ -35,6 +35,8 @@ struct LMState {
   float chib, ab, bb;  // chi^2, alpha, beta at best
   int it;
   bool trial, first, small;
+  int tb;           // first lane of the group's team in this warp (lane-split divisions)
+  unsigned tmask;   // the team's lanes
 };
 
 template <int P>
@@ -112,7 +114,11 @@ __device__ __forceinline__ bool lm_step(LMState<P>& s, const Eval<P>& E, const C
       if constexpr (P == 5) {
         solved = solve_pivot5(jtj, rhs, s.lam, delta);
       } else {
+#if SF_TEAM_SOLVE
+        solved = solve_step_team<P>(jtj, rhs, s.lam, delta, s.tb, s.tmask);
+#else
         solved = solve_step<P>(jtj, rhs, s.lam, delta);
+#endif
       }
       if (solved) {
         double v[P];
@@ -189,6 +195,7 @@ struct LaneSetup {
   int64_t ngroups;
   uint32_t own;   // owned-pixel mask, bit j (chain j < ch, tail ch + t)
   int base, tbase, ch, tl;
+  LaneGeo lg;
 
   // pixel index of slot j (chain: base + 8 j, tail: tbase + j - ch), or -1 if not owned
   __device__ __forceinline__ int off(int j) const {
@@ -218,12 +225,23 @@ struct LaneSetup {
       const bool o = j < ch ? j < nc : (j - ch) < nt;
       own |= (o ? 1u : 0u) << j;
     }
-    // coordinates table: rows written by the lanes of the CTA's first group
-    if (threadIdx.x < LANES) {
+    lg.gl = gl;
+    lg.basef = (float)base;
+    lg.tbasef = (float)tbase;
+    lg.Wf = (float)geom.W;
+    lg.invW = 1.0f / (float)geom.W;
+    // coordinate table (single-warp groups): rows written by the lanes of the CTA's first group
+    if (SLOTS < 8 && threadIdx.x < LANES) {
       for (int j = 0; j < ch + tl; ++j) {
-        const int pp = off(j) < 0 ? 0 : off(j);
-        S.row[j].xy[gl] = make_float2((float)(pp % geom.W), (float)(pp / geom.W));
+        const int o = off(j);
+        const int pp = o < 0 ? 0 : o;
+        S.row[j].xy[SLOTS >= 8 ? 0 : gl] = make_float2((float)(pp % geom.W), (float)(pp / geom.W));
       }
+    }
+    // both pixel buffers start at 0 (slots a lane does not own stay 0 forever)
+    for (int j = 0; j < ch + tl; ++j) {
+      S.row[j].gb[0][threadIdx.x] = 0.0f;
+      S.row[j].gb[1][threadIdx.x] = 0.0f;
     }
     __syncthreads();
   }
@@ -231,7 +249,9 @@ struct LaneSetup {
 
 template <int P, int SLOTS>
 __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
-                                  SLOTS >= 8 ? 1 : (P == 3 ? SF_MINB_P3 : (P == 4 ? SF_MINB_P4 : 2)))
+                                  P == 5 ? (SLOTS >= 8 ? 1 : 2)
+                                         : (SLOTS == 8 ? 2 * SF_MINB_P3 : (SLOTS == 16 ? SF_MINB_P3
+                                                                                     : (P == 3 ? SF_MINB_P3 : SF_MINB_P4))))
     fit_kernel(const float* __restrict__ images, const float* __restrict__ inits, int64_t count, const Geom geom,
                const Cfg cfg, FitOut out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -250,28 +270,33 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
     constexpr int LANES = 8 * SLOTS;
     const int gib = SLOTS >= 8 ? 0 : (threadIdx.x >> 5) * (32 / LANES) + (threadIdx.x & 31) / LANES;
     s.sys = S.sys[gib];
+    constexpr int TEAM = LANES < 32 ? LANES : 32;
+    s.tb = team_base<SLOTS>();
+    s.tmask = TEAM == 32 ? kFull : ((1u << TEAM) - 1u) << s.tb;
   }
   int64_t spot = L.gid - L.ngroups;
   bool need = true, exhausted = false;
   unsigned n_g = 0, n_t = 0, n_e = 0;
 
-  // Next-spot prefetch: the pixels land in PixRow::gpre via cp.async while the
-  // current spot iterates, the init in registers; consumed at the next refill.
+  // Next-spot prefetch: the pixels land in the idle half of the PixRow::gb double
+  // buffer via cp.async while the current spot iterates, the init in registers;
+  // a refill only waits for this lane's copies and flips the buffer index gp.
   float nxt[P];
-  auto prefetch = [&](int64_t sp) {
+  int gp = 1;  // current buffer; the first refill flips to 0
+  auto prefetch = [&](int64_t sp, int buf) {
     if (sp < count) {
       const float* img = images + sp * (int64_t)N;
 #pragma unroll 4
       for (int j = 0; j < L.ch + L.tl; ++j) {
         const int o = L.off(j);
-        if (o >= 0) cp_async4(&S.row[j].gpre[tid], img + o);
+        if (o >= 0) cp_async4(&S.row[j].gb[buf][tid], img + o);
       }
 #pragma unroll
       for (int k = 0; k < P; ++k) nxt[k] = __ldg(inits + sp * P + k);
     }
     cp_async_commit();
   };
-  prefetch(L.gid);
+  prefetch(L.gid, 0);
 
 #pragma unroll 1
   for (;;) {
@@ -289,12 +314,7 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
       bool bad = false;
       if (load) {
         cp_async_wait_all();  // this lane's prefetched pixels of `spot` have landed
-#pragma unroll 4
-        for (int j = 0; j < L.ch + L.tl; ++j) {
-          const float v = L.off(j) >= 0 ? S.row[j].gpre[tid] : 0.0f;
-          S.row[j].gv[tid] = v;
-          bad = bad || !isfinite(v);
-        }
+        gp ^= 1;
         float init[P];
         double v[P];
 #pragma unroll
@@ -303,7 +323,7 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
           bad = bad || !isfinite(init[k]);
           v[k] = (double)init[k];
         }
-        prefetch(spot + L.ngroups);
+        prefetch(spot + L.ngroups, gp ^ 1);
         limit_params<P>(cfg, v, s.p);  // SPEC.md:211 "sigma within bounds after limit"
         s.lam = cfg.lam0;
         s.it = 0;
@@ -315,8 +335,10 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
           for (int k = 0; k < P; ++k) s.p[k] = init[k];
         }
       }
-      const bool gbad = group_any<SLOTS>(bad);
-      const double gsum = pixel_sum<P, SLOTS>(S, L.ch, L.tl);
+      // G = sum g (model.py:223); it is non-finite iff some pixel is (a sum of <= 1024 finite
+      // f32 values cannot overflow f64), so it doubles as the InvalidInput pixel check
+      const double gsum = pixel_sum<P, SLOTS>(S, L.ch, L.tl, gp);
+      const bool gbad = bad || !isfinite(gsum);
       if (load) {
         G = gsum;
         if (gbad) {
@@ -334,9 +356,9 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
 
     Eval<P> E;
     if constexpr (P == 5) {
-      evaluate_explicit5<SLOTS>(S, L.gl, L.own, L.ch, L.tl, s.p, E);
+      evaluate_explicit5<SLOTS>(S, L.lg, L.own, L.ch, L.tl, gp, s.p, E);
     } else {
-      evaluate<P, SLOTS>(S, L.gl, L.own, L.ch, L.tl, G, n, s.p, E);
+      evaluate<P, SLOTS>(S, L.lg, L.own, L.ch, L.tl, gp, G, n, s.p, E);
     }
     if (!exhausted && !skip) {
       n_e += 1;
@@ -365,14 +387,14 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>())
   const bool valid = L.gid < count;
   const int64_t spot = valid ? L.gid : 0;
   const float* img = images + spot * (int64_t)N;
-  for (int j = 0; j < L.ch + L.tl; ++j) S.row[j].gv[tid] = (L.off(j) >= 0 && valid) ? __ldg(img + L.off(j)) : 0.0f;
+  for (int j = 0; j < L.ch + L.tl; ++j) S.row[j].gb[0][tid] = (L.off(j) >= 0 && valid) ? __ldg(img + L.off(j)) : 0.0f;
   float pe[P];
 #pragma unroll
   for (int k = 0; k < P; ++k) pe[k] = valid ? __ldg(params + spot * P + k) : 1.0f;
-  const double G = pixel_sum<P, SLOTS>(S, L.ch, L.tl);
+  const double G = pixel_sum<P, SLOTS>(S, L.ch, L.tl, 0);
   Eval<P> E;
   EvalExtras<P> X;
-  evaluate<P, SLOTS, true>(S, L.gl, L.own, L.ch, L.tl, G, (double)N, pe, E, &X);
+  evaluate<P, SLOTS, true>(S, L.lg, L.own, L.ch, L.tl, 0, G, (double)N, pe, E, &X);
   if (valid && L.gl == 0) {
     sf_eval_record r;
     r.singular = E.singular ? 1 : 0;
