@@ -417,6 +417,14 @@ def run_ours(args):
     hbm_bytes = count * (4 * N + 4 * model) + count * (4 * model + 12 + 2)
     f2f_per_pix = {3: 22, 4: 30, 5: 21}[model]
     f2f_ops = N * n_k * f2f_per_pix
+    traffic = None  # DRAM bytes per launch from the committed ncu capture of this kernel (profiles/)
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            t = json.load(f)
+        if model == 3 and (W, H) == (15, 15):
+            traffic = t["bytes_per_spot"] * count
+    except (OSError, KeyError, ValueError):
+        pass
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "fits/s", "n_gpus": world, "steps": args.steps,
@@ -428,7 +436,9 @@ def run_ours(args):
                        "model": model, "parallelism": f"independent shards x{world}",
                        "l2": f"inputs {count * N * 4 / 1e6:.0f} MB/GPU > 126 MB L2 (no flush needed)"},
             "roofline": {"bound": "fp32", "achieved": achieved / 1e12, "peak": fp32_peak / 1e12, "unit": "TOP/s",
-                         "frac": achieved / fp32_peak, "traffic": None,
+                         "frac": achieved / fp32_peak, "traffic": traffic,
+                         "traffic_note": "DRAM bytes per launch (ncu dram__bytes_read+write, profiles/ncu_traffic.json) "
+                                         f"vs {hbm_bytes:.4g} algorithmic bytes",
                          "ops_per_fit": ops / count, "def": "SURVEY 8d: N*(67*n_G + 18*n_T) algorithmic ops per fit; "
                                                             "peak = SMs*128*sm_max_mhz (FP32 lanes)",
                          "sfu": {"achieved": exps / launch_s / 1e12, "peak": sfu_peak / 1e12,
