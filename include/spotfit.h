@@ -94,6 +94,17 @@ int sf_fit_batch(const float* images, int32_t width, int32_t height, int64_t cou
                  sf_stats* stats);
 
 /*
+ * sf_fit_batch_u16 -- sf_fit_batch for 16-bit camera counts: images [count][H][W]
+ * uint16 (host pointers).  Each chunk is copied as u16 (half the PCIe bytes of
+ * f32) and widened to f32 on the device (exact), so results are identical to
+ * sf_fit_batch on the same values as float32.
+ */
+int sf_fit_batch_u16(const uint16_t* images, int32_t width, int32_t height, int64_t count, const float* inits,
+                     const sf_config* cfg, float* out_params, float* out_alpha, float* out_beta, float* out_nchi2,
+                     uint8_t* out_status, uint8_t* out_iters, const int32_t* devices, int32_t n_devices,
+                     sf_stats* stats);
+
+/*
  * sf_fit_batch_device -- the same fit with every pointer in device memory of
  * the current device, launched on `stream` (cudaStream_t, 0 = legacy default),
  * asynchronous.  Used by bench.py for the HBM-resident measurement and by

@@ -96,6 +96,8 @@ _vp, _i32, _i64, _f64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.
 SYMBOLS = {
     "sf_fit_batch": (ctypes.c_int, [_vp, _i32, _i32, _i64, _vp, ctypes.POINTER(sf_config), _vp, _vp, _vp, _vp, _vp,
                                     _vp, _vp, _i32, ctypes.POINTER(sf_stats)]),
+    "sf_fit_batch_u16": (ctypes.c_int, [_vp, _i32, _i32, _i64, _vp, ctypes.POINTER(sf_config), _vp, _vp, _vp, _vp,
+                                        _vp, _vp, _vp, _i32, ctypes.POINTER(sf_stats)]),
     "sf_fit_batch_device": (ctypes.c_int, [_vp, _i32, _i32, _i64, _vp, ctypes.POINTER(sf_config), _vp, _vp, _vp, _vp,
                                            _vp, _vp, _vp, _vp]),
     "sf_eval_batch_device": (ctypes.c_int, [_vp, _i32, _i32, _i64, _i32, _vp, _vp, _vp]),

@@ -98,7 +98,9 @@ def _as_image_array(images, grid: Optional[PixelGrid]):
         if any(im.grid != grid for im in images):
             raise ValueError("all images in a batch must share one grid (SPEC.md:377)")
         return np.stack([im.values for im in images]), grid
-    a = np.asarray(images, dtype=np.float32)
+    a = np.asarray(images)
+    if a.dtype != np.uint16:  # 16-bit camera counts stream as u16 (sf_fit_batch_u16); everything else as f32
+        a = np.asarray(a, dtype=np.float32)
     if grid is None:
         if a.ndim != 3:
             raise ValueError("images must be (count, H, W), a list of SpotImage, or pass grid=")
@@ -158,7 +160,7 @@ def fit_batch(images, inits=None, config: FitConfig = FitConfig(), engine: str =
     if inits is None:
         import torch
 
-        ini = _auto_inits(torch.as_tensor(imgs).cuda(), grid, P, config).cpu().numpy()
+        ini = _auto_inits(torch.as_tensor(imgs.astype(np.float32, copy=False)).cuda(), grid, P, config).cpu().numpy()
     else:
         ini = np.ascontiguousarray(params_array(inits), dtype=np.float32).reshape(count, P)
     if out is None:
@@ -167,7 +169,8 @@ def fit_batch(images, inits=None, config: FitConfig = FitConfig(), engine: str =
     st = _lib.sf_stats()
     devs = list(devices) if devices else [0]
     dev_arr = (ctypes.c_int32 * len(devs))(*devs)
-    _lib.check(L.sf_fit_batch(_ptr(imgs), grid.width, grid.height, count, _ptr(ini), ctypes.byref(ccfg),
+    entry = L.sf_fit_batch_u16 if imgs.dtype == np.uint16 else L.sf_fit_batch
+    _lib.check(entry(_ptr(imgs), grid.width, grid.height, count, _ptr(ini), ctypes.byref(ccfg),
                               _ptr(out.params), _ptr(out.alpha), _ptr(out.beta), _ptr(out.nchi2), _ptr(out.status),
                               _ptr(out.iterations), dev_arr, len(devs), ctypes.byref(st)))
     out.stats = dict(n_gradient_evals=st.n_gradient_evals, n_trial_evals=st.n_trial_evals,

@@ -131,6 +131,7 @@ struct Slot {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[4] = {};  // start, h2d done, kernel done, d2h done
   float* d_img = nullptr;
+  uint16_t* d_img16 = nullptr;  // 16-bit chunk before widening (sf_fit_batch_u16)
   float* d_init = nullptr;
   float* d_par = nullptr;
   float* d_a = nullptr;
@@ -164,10 +165,11 @@ DevCtx* ctx_for(int dev) {
 }
 
 void free_slot_buffers(Slot& s) {
-  cudaFree(s.d_img); cudaFree(s.d_init); cudaFree(s.d_par); cudaFree(s.d_a); cudaFree(s.d_b); cudaFree(s.d_c);
+  cudaFree(s.d_img); cudaFree(s.d_img16); cudaFree(s.d_init); cudaFree(s.d_par); cudaFree(s.d_a); cudaFree(s.d_b); cudaFree(s.d_c);
   cudaFree(s.d_st); cudaFree(s.d_it);
   cudaFreeHost(s.h_in); cudaFreeHost(s.h_out);
   s.d_img = s.d_init = s.d_par = s.d_a = s.d_b = s.d_c = nullptr;
+  s.d_img16 = nullptr;
   s.d_st = s.d_it = nullptr;
   s.h_in = s.h_out = nullptr;
   s.cap_spots = 0;
@@ -188,6 +190,7 @@ int ensure_ctx(DevCtx& c, int dev, size_t spots, int npix, int P, bool staging) 
     if (!grow) continue;
     free_slot_buffers(s);
     SF_CUDA(cudaMalloc(&s.d_img, spots * npix * sizeof(float)));
+    SF_CUDA(cudaMalloc(&s.d_img16, spots * npix * sizeof(uint16_t)));
     SF_CUDA(cudaMalloc(&s.d_init, spots * kMaxP * sizeof(float)));
     SF_CUDA(cudaMalloc(&s.d_par, spots * kMaxP * sizeof(float)));
     SF_CUDA(cudaMalloc(&s.d_a, spots * sizeof(float)));
@@ -230,6 +233,7 @@ bool is_pinned_ptr(const void* p) {
 
 struct HostJob {
   const float* images;
+  const uint16_t* images16;  // non-null: 16-bit input, widened to f32 on the device
   const float* inits;
   int W, H, P;
   int64_t lo, hi;
@@ -291,15 +295,21 @@ int run_shard(int dev, HostJob& j) {
       copy_out_staged(s, j);
     }
     SF_CUDA(cudaEventRecord(s.ev[0], s.stream));
-    const float* src_img = j.images + lo * N;
+    const size_t px_bytes = j.images16 ? sizeof(uint16_t) : sizeof(float);
+    const void* src_img = j.images16 ? (const void*)(j.images16 + lo * N) : (const void*)(j.images + lo * N);
     const float* src_init = j.inits + lo * P;
     if (!j.pinned_in) {
-      std::memcpy(s.h_in, src_img, n * N * sizeof(float));
+      std::memcpy(s.h_in, src_img, n * N * px_bytes);
       std::memcpy(s.h_in + s.cap_spots * N, src_init, n * P * sizeof(float));
       src_img = s.h_in;
       src_init = s.h_in + s.cap_spots * N;
     }
-    SF_CUDA(cudaMemcpyAsync(s.d_img, src_img, n * N * sizeof(float), cudaMemcpyHostToDevice, s.stream));
+    if (j.images16) {
+      SF_CUDA(cudaMemcpyAsync(s.d_img16, src_img, n * N * px_bytes, cudaMemcpyHostToDevice, s.stream));
+      SF_CUDA(sf::launch_widen_u16(s.d_img16, s.d_img, n * N, s.stream));
+    } else {
+      SF_CUDA(cudaMemcpyAsync(s.d_img, src_img, n * N * px_bytes, cudaMemcpyHostToDevice, s.stream));
+    }
     SF_CUDA(cudaMemcpyAsync(s.d_init, src_init, n * P * sizeof(float), cudaMemcpyHostToDevice, s.stream));
     SF_CUDA(cudaEventRecord(s.ev[1], s.stream));
     sf::LaunchFit a;
@@ -471,10 +481,34 @@ int sf_estimate_initial_device(const float* d_images, int32_t width, int32_t hei
   return 0;
 }
 
+static int fit_batch_impl(const float* images, const uint16_t* images16, int32_t width, int32_t height,
+                          int64_t count, const float* inits, const sf_config* cfg, float* out_params,
+                          float* out_alpha, float* out_beta, float* out_nchi2, uint8_t* out_status, uint8_t* out_iters,
+                          const int32_t* devices, int32_t n_devices, sf_stats* stats);
+
 int sf_fit_batch(const float* images, int32_t width, int32_t height, int64_t count, const float* inits,
                  const sf_config* cfg, float* out_params, float* out_alpha, float* out_beta, float* out_nchi2,
                  uint8_t* out_status, uint8_t* out_iters, const int32_t* devices, int32_t n_devices,
                  sf_stats* stats) {
+  return fit_batch_impl(images, nullptr, width, height, count, inits, cfg, out_params, out_alpha, out_beta, out_nchi2,
+                        out_status, out_iters, devices, n_devices, stats);
+}
+
+int sf_fit_batch_u16(const uint16_t* images, int32_t width, int32_t height, int64_t count, const float* inits,
+                     const sf_config* cfg, float* out_params, float* out_alpha, float* out_beta, float* out_nchi2,
+                     uint8_t* out_status, uint8_t* out_iters, const int32_t* devices, int32_t n_devices,
+                     sf_stats* stats) {
+  if (images && is_device_ptr(images, nullptr)) return fail("sf_fit_batch_u16 takes host images");
+  return fit_batch_impl(nullptr, images, width, height, count, inits, cfg, out_params, out_alpha, out_beta,
+                        out_nchi2, out_status, out_iters, devices, n_devices, stats);
+}
+
+}  // extern "C"
+
+static int fit_batch_impl(const float* images, const uint16_t* images16, int32_t width, int32_t height,
+                          int64_t count, const float* inits, const sf_config* cfg, float* out_params,
+                          float* out_alpha, float* out_beta, float* out_nchi2, uint8_t* out_status, uint8_t* out_iters,
+                          const int32_t* devices, int32_t n_devices, sf_stats* stats) {
   const auto t0 = std::chrono::steady_clock::now();
   if (check_grid(width, height) != 0) return -1;
   if (count < 0) return fail("negative count");
@@ -482,7 +516,8 @@ int sf_fit_batch(const float* images, int32_t width, int32_t height, int64_t cou
   if (make_cfg(cfg, width, height, kc) != 0) return -1;
   if (stats) std::memset(stats, 0, sizeof(*stats));
   if (count == 0) return 0;
-  if (!images || !inits || !out_params || !out_alpha || !out_beta || !out_nchi2 || !out_status || !out_iters)
+  if ((!images && !images16) || !inits || !out_params || !out_alpha || !out_beta || !out_nchi2 || !out_status ||
+      !out_iters)
     return fail("NULL buffer");
   int ndev_avail = sf_device_count();
   if (ndev_avail < 1) return fail("no CUDA device available (the CUDA engine has no CPU fallback)");
@@ -496,7 +531,7 @@ int sf_fit_batch(const float* images, int32_t width, int32_t height, int64_t cou
     devs.push_back(0);
   }
   int dptr_dev = -1;
-  if (is_device_ptr(images, &dptr_dev)) {
+  if (images && is_device_ptr(images, &dptr_dev)) {
     // device-resident batch: one device, synchronous call on the library stream
     if (devs.size() > 1) return fail("device-pointer batches run on the owning device only");
     SF_CUDA(cudaSetDevice(dptr_dev));
@@ -526,7 +561,7 @@ int sf_fit_batch(const float* images, int32_t width, int32_t height, int64_t cou
     }
     return 0;
   }
-  const bool pin_in = is_pinned_ptr(images) && is_pinned_ptr(inits);
+  const bool pin_in = is_pinned_ptr(images ? (const void*)images : (const void*)images16) && is_pinned_ptr(inits);
   const bool pin_out = is_pinned_ptr(out_params) && is_pinned_ptr(out_alpha) && is_pinned_ptr(out_beta) &&
                        is_pinned_ptr(out_nchi2) && is_pinned_ptr(out_status) && is_pinned_ptr(out_iters);
   const int nd = (int)devs.size();
@@ -534,6 +569,7 @@ int sf_fit_batch(const float* images, int32_t width, int32_t height, int64_t cou
   for (int d = 0; d < nd; ++d) {
     HostJob& j = jobs[d];
     j.images = images;
+    j.images16 = images16;
     j.inits = inits;
     j.W = width;
     j.H = height;
@@ -573,5 +609,3 @@ int sf_fit_batch(const float* images, int32_t width, int32_t height, int64_t cou
   }
   return 0;
 }
-
-}  // extern "C"
