@@ -189,7 +189,8 @@ int sf_lane_geometry(int32_t width, int32_t height, int32_t* slots, int32_t* ppl
 /*
  * sf_debug_npexp_device -- diagnostic: the kernel's float32 exp (numpy's
  * simd_exp_f32 restated; model.py:177,193 call np.exp) on a device array.
- * variant 0: production (fast-path IEEE division); 1: CUDA __fdiv_rn.
+ * variant 0: production (fast-path IEEE division); 1: CUDA __fdiv_rn;
+ * 2: the packed f32x2 form used by the fit kernel's chain loops.
  */
 int sf_debug_npexp_device(const float* d_x, float* d_y, int64_t n, int32_t variant, void* stream);
 

@@ -379,7 +379,7 @@ int sf_simulate_device(const sf_sim_config* cfg, int32_t width, int32_t height, 
 }
 
 int sf_debug_npexp_device(const float* d_x, float* d_y, int64_t n, int32_t variant, void* stream) {
-  if (n < 0 || (variant != 0 && variant != 1)) return fail("bad arguments");
+  if (n < 0 || variant < 0 || variant > 2) return fail("bad arguments");
   cudaError_t e = sf::launch_npexp(d_x, d_y, n, variant, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail("npexp launch failed: %s", cudaGetErrorString(e));
   return 0;

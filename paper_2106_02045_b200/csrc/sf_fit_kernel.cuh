@@ -230,12 +230,24 @@ struct LaneSetup {
     lg.tbasef = (float)tbase;
     lg.Wf = (float)geom.W;
     lg.invW = 1.0f / (float)geom.W;
-    // coordinate table (single-warp groups): rows written by the lanes of the CTA's first group
+    lg.nz2 = geom.nz2;
+    // coordinate table (single-warp groups): rows written by the lanes of the CTA's first group.
+    // Chain slot pairs (j even, j + 1 < ch) of the implicit models use the pair layout of
+    // sf_device.cuh:pair_xy (row j: x of slots j, j+1; row j+1: their y), all other rows (x, y).
     if (SLOTS < 8 && threadIdx.x < LANES) {
-      for (int j = 0; j < ch + tl; ++j) {
+      const int ch2 = P == 5 ? 0 : (ch & ~1);
+      auto xy = [&](int j) {
         const int o = off(j);
         const int pp = o < 0 ? 0 : o;
-        S.row[j].xy[SLOTS >= 8 ? 0 : gl] = make_float2((float)(pp % geom.W), (float)(pp / geom.W));
+        return make_float2((float)(pp % geom.W), (float)(pp / geom.W));
+      };
+      for (int j = 0; j < ch + tl; ++j) {
+        if (j < ch2) {
+          const float2 a = xy(j & ~1), b = xy(j | 1);
+          S.row[j].xy[SLOTS >= 8 ? 0 : gl] = (j & 1) ? make_float2(a.y, b.y) : make_float2(a.x, b.x);
+        } else {
+          S.row[j].xy[SLOTS >= 8 ? 0 : gl] = xy(j);
+        }
       }
     }
     // both pixel buffers start at 0 (slots a lane does not own stay 0 forever)
@@ -247,7 +259,7 @@ struct LaneSetup {
   }
 };
 
-template <int P, int SLOTS>
+template <int P, int SLOTS, bool FULL>
 __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
                                   P == 5 ? (SLOTS >= 8 ? 1 : 2)
                                          : (SLOTS == 8 ? 2 * SF_MINB_P3 : (SLOTS == 16 ? SF_MINB_P3
@@ -276,6 +288,7 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
   }
   int64_t spot = L.gid - L.ngroups;
   bool need = true, exhausted = false;
+  bool lane_gt = true, lane_g40 = true, warp_gt = true;  // spot tameness (pixel_sum)
   unsigned n_g = 0, n_t = 0, n_e = 0;
 
   // Next-spot prefetch: the pixels land in the idle half of the PixRow::gb double
@@ -337,8 +350,14 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
       }
       // G = sum g (model.py:223); it is non-finite iff some pixel is (a sum of <= 1024 finite
       // f32 values cannot overflow f64), so it doubles as the InvalidInput pixel check
-      const double gsum = pixel_sum<P, SLOTS>(S, L.ch, L.tl, gp);
+      bool sgt, sg40;
+      const double gsum = pixel_sum<P, SLOTS>(S, L.ch, L.tl, gp, sgt, sg40);
       const bool gbad = bad || !isfinite(gsum);
+      if (load) {
+        lane_gt = sgt;
+        lane_g40 = sg40;
+      }
+      warp_gt = __all_sync(kFull, lane_gt || exhausted);
       if (load) {
         G = gsum;
         if (gbad) {
@@ -358,7 +377,7 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
     if constexpr (P == 5) {
       evaluate_explicit5<SLOTS>(S, L.lg, L.own, L.ch, L.tl, gp, s.p, E);
     } else {
-      evaluate<P, SLOTS>(S, L.lg, L.own, L.ch, L.tl, gp, G, n, s.p, E);
+      evaluate<P, SLOTS, FULL>(S, L.lg, L.own, L.ch, L.tl, gp, G, n, s.p, warp_gt, lane_g40, !exhausted && !skip, E);
     }
     if (!exhausted && !skip) {
       n_e += 1;
@@ -373,7 +392,7 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
 }
 
 // Model-level evaluation (sf_eval_batch_device): one group per spot, no LM.
-template <int P, int SLOTS>
+template <int P, int SLOTS, bool FULL>
 __global__ void __launch_bounds__(threads_per_block<SLOTS>())
     eval_kernel(const float* __restrict__ images, const float* __restrict__ params, int64_t count, const Geom geom,
                 sf_eval_record* __restrict__ out) {
@@ -391,10 +410,11 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>())
   float pe[P];
 #pragma unroll
   for (int k = 0; k < P; ++k) pe[k] = valid ? __ldg(params + spot * P + k) : 1.0f;
-  const double G = pixel_sum<P, SLOTS>(S, L.ch, L.tl, 0);
+  bool gt, g40;
+  const double G = pixel_sum<P, SLOTS>(S, L.ch, L.tl, 0, gt, g40);
   Eval<P> E;
   EvalExtras<P> X;
-  evaluate<P, SLOTS, true>(S, L.lg, L.own, L.ch, L.tl, 0, G, (double)N, pe, E, &X);
+  evaluate<P, SLOTS, FULL, true>(S, L.lg, L.own, L.ch, L.tl, 0, G, (double)N, pe, __all_sync(kFull, gt), g40, true, E, &X);
   if (valid && L.gl == 0) {
     sf_eval_record r;
     r.singular = E.singular ? 1 : 0;

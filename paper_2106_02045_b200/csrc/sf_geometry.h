@@ -63,6 +63,9 @@ inline int build_geom(int W, int H, int P, Geom& g, int* ch_need = nullptr, int*
   }
   g.ch = chn;
   g.tl = tln;
+  g.full = 1;
+  for (int l = 0; l < g.lanes; ++l) g.full = g.full && g.nc[l] == chn;
+  g.nz2 = 0x8000000080000000ull;
   if (ch_need) *ch_need = chn;
   if (tl_need) *tl_need = tln;
   return ppl;

@@ -111,15 +111,29 @@ cudaError_t launch_widen_u16(const uint16_t* in, float* out, int64_t n, cudaStre
 }
 
 // Exhaustive-check helper: numpy exp on the device (variant 0: production
-// npexp, 1: the same with CUDA's IEEE __fdiv_rn).
-__global__ void npexp_kernel(const float* __restrict__ x, float* __restrict__ y, int64_t n, int variant) {
+// scalar npexp, 1: the same with CUDA's IEEE __fdiv_rn, 2: the packed f32x2
+// npexp2 of the chain loops, on element pairs (x[2i], x[2i+1])).
+__global__ void npexp_kernel(const float* __restrict__ x, float* __restrict__ y, int64_t n, int variant,
+                             unsigned long long nz2) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (variant == 2) {
+    const int64_t a = 2 * i;
+    if (a < n) {
+      const float xa = x[a], xb = a + 1 < n ? x[a + 1] : 0.0f;
+      float ya, yb;
+      up2(npexp2(pk2(xa, xb), f2{nz2}), ya, yb);
+      y[a] = ya;
+      if (a + 1 < n) y[a + 1] = yb;
+    }
+    return;
+  }
   if (i < n) y[i] = variant == 0 ? npexp(x[i]) : npexp_ieee_div(x[i]);
 }
 
 cudaError_t launch_npexp(const float* x, float* y, int64_t n, int variant, cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
-  npexp_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(x, y, n, variant);
+  const int64_t threads = variant == 2 ? (n + 1) / 2 : n;
+  npexp_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, stream>>>(x, y, n, variant, 0x8000000080000000ull);
   return cudaGetLastError();
 }
 
