@@ -197,6 +197,10 @@ struct LaneSetup {
   int base, tbase, ch, tl;
   LaneGeo lg;
 
+  // group index within the CTA
+  __device__ __forceinline__ int gib() const {
+    return SLOTS >= 8 ? 0 : (threadIdx.x >> 5) * (32 / (8 * SLOTS)) + (threadIdx.x & 31) / (8 * SLOTS);
+  }
   // pixel index of slot j (chain: base + 8 j, tail: tbase + j - ch), or -1 if not owned
   __device__ __forceinline__ int off(int j) const {
     return owns(own, j) ? (j < ch ? base + 8 * j : tbase + (j - ch)) : -1;
@@ -231,30 +235,23 @@ struct LaneSetup {
     lg.Wf = (float)geom.W;
     lg.invW = 1.0f / (float)geom.W;
     lg.nz2 = geom.nz2;
-    // coordinate table (single-warp groups): rows written by the lanes of the CTA's first group.
-    // Chain slot pairs (j even, j + 1 < ch) of the implicit models use the pair layout of
-    // sf_device.cuh:pair_xy (row j: x of slots j, j+1; row j+1: their y), all other rows (x, y).
+    // coordinate table (single-warp groups), written by the lanes of the CTA's first group:
+    // pair rows hold (x_A, x_B, y_A, y_B) of chain slots (2i, 2i+1), solo rows (x, y)
     if (SLOTS < 8 && threadIdx.x < LANES) {
-      const int ch2 = P == 5 ? 0 : (ch & ~1);
       auto xy = [&](int j) {
         const int o = off(j);
         const int pp = o < 0 ? 0 : o;
         return make_float2((float)(pp % geom.W), (float)(pp / geom.W));
       };
-      for (int j = 0; j < ch + tl; ++j) {
-        if (j < ch2) {
-          const float2 a = xy(j & ~1), b = xy(j | 1);
-          S.row[j].xy[SLOTS >= 8 ? 0 : gl] = (j & 1) ? make_float2(a.y, b.y) : make_float2(a.x, b.x);
-        } else {
-          S.row[j].xy[SLOTS >= 8 ? 0 : gl] = xy(j);
-        }
+      for (int i = 0; i < ch / 2; ++i) {
+        const float2 a = xy(2 * i), b = xy(2 * i + 1);
+        S.pr[i].xy[SLOTS >= 8 ? 0 : gl] = make_float4(a.x, b.x, a.y, b.y);
       }
+      for (int j = ch & ~1; j < ch + tl; ++j) S.so[j - (ch & ~1)].xy[SLOTS >= 8 ? 0 : gl] = xy(j);
     }
-    // both pixel buffers start at 0 (slots a lane does not own stay 0 forever)
-    for (int j = 0; j < ch + tl; ++j) {
-      S.row[j].gb[0][threadIdx.x] = 0.0f;
-      S.row[j].gb[1][threadIdx.x] = 0.0f;
-    }
+    // pixel values start at 0 (load_spot rewrites a group's slots on every refill)
+    for (int i = 0; i < ch / 2; ++i) S.pr[i].g[threadIdx.x] = make_float2(0.0f, 0.0f);
+    for (int r = 0; r < (ch & 1) + tl; ++r) S.so[r].g[threadIdx.x] = 0.0f;
     __syncthreads();
   }
 };
@@ -268,10 +265,9 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
                const Cfg cfg, FitOut out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem<P, SLOTS> S;
-  S.bind(smem_raw);
+  S.bind(smem_raw, geom.ch, geom.tl, geom.N);
   LaneSetup<P, SLOTS> L;
   L.init(S, geom);
-  const int tid = threadIdx.x;
   const bool leader = L.gl == 0;
   const int N = geom.N;
   const double n = (double)N;
@@ -280,8 +276,7 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
   LMState<P> s;
   {
     constexpr int LANES = 8 * SLOTS;
-    const int gib = SLOTS >= 8 ? 0 : (threadIdx.x >> 5) * (32 / LANES) + (threadIdx.x & 31) / LANES;
-    s.sys = S.sys[gib];
+    s.sys = S.sys[L.gib()];
     constexpr int TEAM = LANES < 32 ? LANES : 32;
     s.tb = team_base<SLOTS>();
     s.tmask = TEAM == 32 ? kFull : ((1u << TEAM) - 1u) << s.tb;
@@ -291,29 +286,27 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
   bool lane_gt = true, lane_g40 = true, warp_gt = true;  // spot tameness (pixel_sum)
   unsigned n_g = 0, n_t = 0, n_e = 0;
 
-  // Next-spot prefetch: the pixels land in the idle half of the PixRow::gb double
-  // buffer via cp.async while the current spot iterates, the init in registers;
-  // a refill only waits for this lane's copies and flips the buffer index gp.
+  // Next-spot prefetch: the group streams the next spot into its staging window
+  // (stage_spot) while the current spot iterates, the init into registers; a
+  // refill waits for the copies, scatters the window into the lanes' pixel
+  // slots (load_spot), then starts the following spot's copy.
   float nxt[P];
-  int gp = 1;  // current buffer; the first refill flips to 0
-  auto prefetch = [&](int64_t sp, int buf) {
+  int nsh = 0;  // float offset of the staged spot inside its window
+  const int gib = L.gib();
+  const uintptr_t lo = (uintptr_t)images, hi = (uintptr_t)(images + count * (int64_t)N);
+  auto prefetch = [&](int64_t sp) {
     if (sp < count) {
-      const float* img = images + sp * (int64_t)N;
-#pragma unroll 4
-      for (int j = 0; j < L.ch + L.tl; ++j) {
-        const int o = L.off(j);
-        if (o >= 0) cp_async4(&S.row[j].gb[buf][tid], img + o);
-      }
+      nsh = stage_spot<P, SLOTS>(S, gib, L.gl, images + sp * (int64_t)N, lo, hi, N);
 #pragma unroll
       for (int k = 0; k < P; ++k) nxt[k] = __ldg(inits + sp * P + k);
     }
     cp_async_commit();
   };
-  prefetch(L.gid, 0);
+  prefetch(L.gid);
 
 #pragma unroll 1
   for (;;) {
-    // Every warp-collective below (votes, shuffles inside pixel_sum and
+    // Every warp-collective below (votes, shuffles inside load_spot and
     // evaluate) is reached by all 32 lanes on every trip: groups only diverge
     // in the LM bookkeeping after the evaluation.
     bool skip = false;  // group refilled with an InvalidInput spot: no LM step this trip
@@ -324,10 +317,10 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
         exhausted = spot >= count;
       }
       const bool load = need && !exhausted;
+      if (load) cp_async_wait_all();  // this lane's copies of `spot` have landed
+      group_sync<SLOTS>();             // ... and every other lane's
       bool bad = false;
       if (load) {
-        cp_async_wait_all();  // this lane's prefetched pixels of `spot` have landed
-        gp ^= 1;
         float init[P];
         double v[P];
 #pragma unroll
@@ -336,7 +329,6 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
           bad = bad || !isfinite(init[k]);
           v[k] = (double)init[k];
         }
-        prefetch(spot + L.ngroups, gp ^ 1);
         limit_params<P>(cfg, v, s.p);  // SPEC.md:211 "sigma within bounds after limit"
         s.lam = cfg.lam0;
         s.it = 0;
@@ -351,7 +343,10 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
       // G = sum g (model.py:223); it is non-finite iff some pixel is (a sum of <= 1024 finite
       // f32 values cannot overflow f64), so it doubles as the InvalidInput pixel check
       bool sgt, sg40;
-      const double gsum = pixel_sum<P, SLOTS>(S, L.ch, L.tl, gp, sgt, sg40);
+      const double gsum =
+          load_spot<P, SLOTS>(S, S.stage + gib * S.sw + nsh, load, L.own, L.base, L.tbase, L.ch, L.tl, sgt, sg40);
+      group_sync<SLOTS>();  // the staging window has been read: refill it
+      if (load) prefetch(spot + L.ngroups);
       const bool gbad = bad || !isfinite(gsum);
       if (load) {
         lane_gt = sgt;
@@ -375,9 +370,9 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
 
     Eval<P> E;
     if constexpr (P == 5) {
-      evaluate_explicit5<SLOTS>(S, L.lg, L.own, L.ch, L.tl, gp, s.p, E);
+      evaluate_explicit5<SLOTS>(S, L.lg, L.own, L.ch, L.tl, s.p, E);
     } else {
-      evaluate<P, SLOTS, FULL>(S, L.lg, L.own, L.ch, L.tl, gp, G, n, s.p, warp_gt, lane_g40, !exhausted && !skip, E);
+      evaluate<P, SLOTS, FULL>(S, L.lg, L.own, L.ch, L.tl, G, n, s.p, warp_gt, lane_g40, !exhausted && !skip, E);
     }
     if (!exhausted && !skip) {
       n_e += 1;
@@ -398,23 +393,28 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>())
                 sf_eval_record* __restrict__ out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem<P, SLOTS> S;
-  S.bind(smem_raw);
+  S.bind(smem_raw, geom.ch, geom.tl, geom.N);
   LaneSetup<P, SLOTS> L;
   L.init(S, geom);
-  const int tid = threadIdx.x;
   const int N = geom.N;
   const bool valid = L.gid < count;
   const int64_t spot = valid ? L.gid : 0;
-  const float* img = images + spot * (int64_t)N;
-  for (int j = 0; j < L.ch + L.tl; ++j) S.row[j].gb[0][tid] = (L.off(j) >= 0 && valid) ? __ldg(img + L.off(j)) : 0.0f;
+  const int gib = L.gib();
+  int sh = 0;
+  if (valid)
+    sh = stage_spot<P, SLOTS>(S, gib, L.gl, images + spot * (int64_t)N, (uintptr_t)images,
+                              (uintptr_t)(images + count * (int64_t)N), N);
+  cp_async_commit();
+  cp_async_wait_all();
+  group_sync<SLOTS>();
   float pe[P];
 #pragma unroll
   for (int k = 0; k < P; ++k) pe[k] = valid ? __ldg(params + spot * P + k) : 1.0f;
   bool gt, g40;
-  const double G = pixel_sum<P, SLOTS>(S, L.ch, L.tl, 0, gt, g40);
+  const double G = load_spot<P, SLOTS>(S, S.stage + gib * S.sw + sh, valid, L.own, L.base, L.tbase, L.ch, L.tl, gt, g40);
   Eval<P> E;
   EvalExtras<P> X;
-  evaluate<P, SLOTS, FULL, true>(S, L.lg, L.own, L.ch, L.tl, 0, G, (double)N, pe, __all_sync(kFull, gt), g40, true, E, &X);
+  evaluate<P, SLOTS, FULL, true>(S, L.lg, L.own, L.ch, L.tl, G, (double)N, pe, __all_sync(kFull, gt), g40, true, E, &X);
   if (valid && L.gl == 0) {
     sf_eval_record r;
     r.singular = E.singular ? 1 : 0;

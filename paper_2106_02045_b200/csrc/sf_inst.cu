@@ -18,7 +18,7 @@ int SF_UNIT_NAME(launch_fit, SF_P, SF_SLOTS)(const LaunchFit& a, cudaError_t* er
   auto kern = (SF_P != 5 && a.geom.full) ? fit_kernel<SF_P, SF_SLOTS, SF_P != 5> : fit_kernel<SF_P, SF_SLOTS, false>;
   constexpr int tpb = threads_per_block<SF_SLOTS>();
   constexpr int groups_per_block = SF_SLOTS >= 8 ? 1 : (tpb / 32) * (32 / (8 * SF_SLOTS));
-  const size_t smem = Smem<SF_P, SF_SLOTS>::bytes(a.geom.ch + a.geom.tl);
+  const size_t smem = Smem<SF_P, SF_SLOTS>::bytes(a.geom.ch, a.geom.tl, a.geom.N);
   *err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (*err != cudaSuccess) return 0;
   int per_sm = 0;
@@ -39,7 +39,7 @@ int SF_UNIT_NAME(launch_eval, SF_P, SF_SLOTS)(const LaunchEval& a, cudaError_t* 
   auto kern = a.geom.full ? eval_kernel<SF_P, SF_SLOTS, true> : eval_kernel<SF_P, SF_SLOTS, false>;
   constexpr int tpb = threads_per_block<SF_SLOTS>();
   constexpr int groups_per_block = SF_SLOTS >= 8 ? 1 : (tpb / 32) * (32 / (8 * SF_SLOTS));
-  const size_t smem = Smem<SF_P, SF_SLOTS>::bytes(a.geom.ch + a.geom.tl);
+  const size_t smem = Smem<SF_P, SF_SLOTS>::bytes(a.geom.ch, a.geom.tl, a.geom.N);
   *err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (*err != cudaSuccess) return 0;
   const int64_t blocks = (a.count + groups_per_block - 1) / groups_per_block;
