@@ -60,37 +60,68 @@ __device__ __forceinline__ void write_result(const FitOut& o, int64_t spot, bool
   o.iters[spot] = (uint8_t)it;
 }
 
+// Post-trial decision of PAPER.md:153-174 (oracle/lm.py:fit_single) for a trial
+// chi^2 `chit` (+inf for StepFailed, NaN for a singular / non-finite trial):
+// returns kRetry (retry the step with the raised lambda), kAccept (the trial is
+// the next iteration's point), or StopReason | flags >= 0 (MaxError is 0; with
+// *at_best: restore best).
+constexpr int kRetry = -1, kAccept = -2;
+template <int P>
+__device__ __forceinline__ int post_trial(LMState<P>& s, const Cfg& c, float chit, bool small, bool* at_best) {
+  if (s.first) {
+    s.first = false;
+    if (s.chib > chit) s.lam = s.lam / c.lam_down;
+  }
+  if (!small && s.chib < chit && s.lam < c.lam_max) {
+    s.lam = s.lam * c.lam_up;
+    return kRetry;
+  }
+  if (isnan(chit) || (s.chib < chit && s.lam >= c.lam_max)) {
+    *at_best = true;
+    return SF_STOP_NOT_CONVERGED;
+  }
+  if (s.chib < chit) {
+    *at_best = true;
+    return SF_STOP_MIN_DELTA | SF_FLAG_NOIMP;
+  }
+  if ((double)chit < c.max_error) return SF_STOP_MAX_ERROR;
+  if ((double)s.chib * (1.0 - c.min_delta) < (double)chit) return SF_STOP_MIN_DELTA;
+  if (small) return SF_STOP_MIN_STEP;
+  if (s.it >= c.max_it) return SF_STOP_MAX_ITERATIONS;
+  return kAccept;
+}
+
 // Consume one evaluation; returns true when the spot's fit has finished (result written).
-// Mirrors oracle/lm.py:fit_single line for line (App. A), with the accepted
-// trial's evaluation reused as the next iteration's G-eval ([A6]).
+// Mirrors oracle/lm.py:fit_single, with the accepted trial's
+// evaluation reused as the next iteration's G-eval ([A6]).  Straight-line
+// decision first, then ONE solve site: every group of the warp that needs a
+// step reaches the (f64-division-bound) damped solve in the same pass, so the
+// warp executes it once per trip instead of once per divergent path.
 template <int P>
 __device__ __forceinline__ bool lm_step(LMState<P>& s, const Eval<P>& E, const Cfg& c, const FitOut& o,
                                         int64_t spot, bool leader, int n_pix, unsigned& n_g, unsigned& n_t) {
   constexpr int T = P * (P + 1) / 2;
-  float chit = 0.0f;
-  bool small = s.small;
   int status = -1;       // StopReason | flags once the fit has finished
   bool at_best = false;  // result is the saved best point (restore) rather than E's point
-  int action;            // 0: process E as G-eval, 1: solve a trial, 2: post-trial decision
+  bool g_eval = !s.trial;
   if (s.trial) {
-    chit = E.singular ? __int_as_float(0x7fc00000) : E.chi;
-    action = 2;
-  } else {
-    action = 0;
+    const float chit = E.singular ? __int_as_float(0x7fc00000) : E.chi;
+    const int d = post_trial<P>(s, c, chit, s.small, &at_best);
+    if (d == kAccept) {
+      s.trial = false;  // accepted, budget left: E is exactly the next iteration's G-eval at s.p
+      g_eval = true;
+    } else if (d >= 0) {
+      status = d;
+    }
   }
-#pragma unroll 1
-  for (;;) {
-    if (action == 0) {
-      s.it += 1;
-      n_g += 1;
-      if (E.singular || !isfinite(E.chi)) {
-        status = SF_STOP_NOT_CONVERGED;
-        break;
-      }
-      if ((double)E.chi < c.max_error) {
-        status = SF_STOP_MAX_ERROR;
-        break;
-      }
+  if (g_eval) {
+    s.it += 1;
+    n_g += 1;
+    if (E.singular || !isfinite(E.chi)) {
+      status = SF_STOP_NOT_CONVERGED;
+    } else if ((double)E.chi < c.max_error) {
+      status = SF_STOP_MAX_ERROR;
+    } else {
       s.chib = E.chi;
       s.ab = E.alpha;
       s.bb = E.beta;
@@ -102,82 +133,44 @@ __device__ __forceinline__ bool lm_step(LMState<P>& s, const Eval<P>& E, const C
 #pragma unroll
       for (int m = 0; m < T; ++m) s.sys[m] = E.jtj[m];
       s.first = true;
-      action = 1;
     }
-    if (action == 1) {  // PAPER.md:147-151 (and the retry body 159-164)
-      double jtj[T], rhs[P], delta[P];
+  }
+  // PAPER.md:147-151 and the retry body 159-164
+#pragma unroll 1
+  while (status < 0) {
+    double jtj[T], rhs[P], delta[P];
 #pragma unroll
-      for (int m = 0; m < T; ++m) jtj[m] = s.sys[m];
+    for (int m = 0; m < T; ++m) jtj[m] = s.sys[m];
 #pragma unroll
-      for (int k = 0; k < P; ++k) rhs[k] = s.sys[T + k];
-      bool solved;
-      if constexpr (P == 5) {
-        solved = solve_pivot5(jtj, rhs, s.lam, delta);
-      } else {
+    for (int k = 0; k < P; ++k) rhs[k] = s.sys[T + k];
+    bool solved;
+    if constexpr (P == 5) {
+      solved = solve_pivot5(jtj, rhs, s.lam, delta);
+    } else {
 #if SF_TEAM_SOLVE
-        solved = solve_step_team<P>(jtj, rhs, s.lam, delta, s.tb, s.tmask);
+      solved = solve_step_team<P>(jtj, rhs, s.lam, delta, s.tb, s.tmask);
 #else
-        solved = solve_step<P>(jtj, rhs, s.lam, delta);
+      solved = solve_step<P>(jtj, rhs, s.lam, delta);
 #endif
-      }
-      if (solved) {
-        double v[P];
-        small = true;
+    }
+    if (solved) {
+      double v[P];
+      bool small = true;
 #pragma unroll
-        for (int k = 0; k < P; ++k) {
-          v[k] = (double)s.best[k] + delta[k];
-          const double thr = c.min_step * fmax(fabs((double)s.best[k]), 1.0);
-          small = small && (fabs(delta[k]) < thr);
-        }
-        limit_params<P>(c, v, s.p);
-        s.small = small;
-        s.trial = true;
-        n_t += 1;
-        return false;  // evaluate the trial point next
+      for (int k = 0; k < P; ++k) {
+        v[k] = (double)s.best[k] + delta[k];
+        const double thr = c.min_step * fmax(fabs((double)s.best[k]), 1.0);
+        small = small && (fabs(delta[k]) < thr);
       }
-      chit = __int_as_float(0x7f800000);  // StepFailed: chi'^2 = +inf, not small
-      small = false;
-      action = 2;
+      limit_params<P>(c, v, s.p);
+      s.small = small;
+      s.trial = true;
+      n_t += 1;
+      return false;  // evaluate the trial point next
     }
-    // action == 2: PAPER.md:153-174
-    if (s.first) {
-      s.first = false;
-      if (s.chib > chit) s.lam = s.lam / c.lam_down;
-    }
-    if (!small && s.chib < chit && s.lam < c.lam_max) {
-      s.lam = s.lam * c.lam_up;
-      action = 1;
-      continue;
-    }
-    if (isnan(chit) || (s.chib < chit && s.lam >= c.lam_max)) {
-      status = SF_STOP_NOT_CONVERGED;
-      at_best = true;
-      break;
-    }
-    if (s.chib < chit) {
-      status = SF_STOP_MIN_DELTA | SF_FLAG_NOIMP;
-      at_best = true;
-      break;
-    }
-    if ((double)chit < c.max_error) {
-      status = SF_STOP_MAX_ERROR;
-      break;
-    }
-    if ((double)s.chib * (1.0 - c.min_delta) < (double)chit) {
-      status = SF_STOP_MIN_DELTA;
-      break;
-    }
-    if (small) {
-      status = SF_STOP_MIN_STEP;
-      break;
-    }
-    if (s.it >= c.max_it) {
-      status = SF_STOP_MAX_ITERATIONS;
-      break;
-    }
-    // accepted, budget left: E is exactly the next iteration's G-eval at s.p
-    s.trial = false;
-    action = 0;
+    // StepFailed: chi'^2 = +inf, not small -> retry with a raised lambda or stop
+    const int d = post_trial<P>(s, c, __int_as_float(0x7f800000), false, &at_best);
+    if (d >= 0) status = d;  // (never kAccept: +inf is not below chi_best)
   }
   float rp[P];
 #pragma unroll
