@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
   LMState<P> s;
   {
     constexpr int LANES = 8 * SLOTS;
-    s.sys = S.sys[L.gib()];
+    s.sys = S.sys + L.gib() * Smem<P, SLOTS>::kSysQ;
     constexpr int TEAM = LANES < 32 ? LANES : 32;
     s.tb = team_base<SLOTS>();
     s.tmask = TEAM == 32 ? kFull : ((1u << TEAM) - 1u) << s.tb;
