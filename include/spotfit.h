@@ -194,6 +194,13 @@ int sf_lane_geometry(int32_t width, int32_t height, int32_t* slots, int32_t* ppl
  */
 int sf_debug_npexp_device(const float* d_x, float* d_y, int64_t n, int32_t variant, void* stream);
 
+/*
+ * sf_debug_ddiv_device -- diagnostic: the kernel's shared-divisor f64 division
+ * (the LDL^T pivots and the alpha/beta denominator of SPEC.md:189-197 and
+ * model.py:226-233, 281-287) on device arrays; must equal IEEE a / b.
+ */
+int sf_debug_ddiv_device(const double* d_a, const double* d_b, double* d_out, int64_t n, void* stream);
+
 int sf_device_count(void);
 const char* sf_last_error(void);
 int sf_version(void);

@@ -106,6 +106,7 @@ SYMBOLS = {
     "sf_simulate_device": (ctypes.c_int, [ctypes.POINTER(sf_sim_config), _i32, _i32, _i64, _i64, _vp, _vp, _vp]),
     "sf_lane_geometry": (ctypes.c_int, [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp]),
     "sf_debug_npexp_device": (ctypes.c_int, [_vp, _vp, _i64, _i32, _vp]),
+    "sf_debug_ddiv_device": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp]),
     "sf_host_alloc": (ctypes.c_void_p, [ctypes.c_size_t]),
     "sf_host_free": (None, [_vp]),
     "sf_device_count": (ctypes.c_int, []),

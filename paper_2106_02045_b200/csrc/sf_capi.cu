@@ -93,7 +93,11 @@ void shape_need(const sf::Geom& g, int* ch, int* tl) {
   }
 }
 
-int dispatch_fit(int P, const sf::LaunchFit& a) {
+int dispatch_fit(int P, const sf::LaunchFit& a_in) {
+  // each launch holds one dynamic-claim counter slot (sf_fit_kernel.cuh:g_work) until it ends
+  static std::atomic<unsigned> next_slot{0};
+  sf::LaunchFit a = a_in;
+  a.out.work_slot = (int)(next_slot.fetch_add(1u) % (unsigned)sf::kWorkSlots);
   cudaError_t err = cudaSuccess;
   int used = -1;
   const int slots = a.geom.slots, ch = a.geom.ch, tl = a.geom.tl;
@@ -382,6 +386,13 @@ int sf_debug_npexp_device(const float* d_x, float* d_y, int64_t n, int32_t varia
   if (n < 0 || variant < 0 || variant > 2) return fail("bad arguments");
   cudaError_t e = sf::launch_npexp(d_x, d_y, n, variant, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail("npexp launch failed: %s", cudaGetErrorString(e));
+  return 0;
+}
+
+int sf_debug_ddiv_device(const double* d_a, const double* d_b, double* d_out, int64_t n, void* stream) {
+  if (n < 0) return fail("bad arguments");
+  cudaError_t e = sf::launch_ddiv(d_a, d_b, d_out, n, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail("ddiv launch failed: %s", cudaGetErrorString(e));
   return 0;
 }
 

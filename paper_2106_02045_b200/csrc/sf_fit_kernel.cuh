@@ -20,7 +20,17 @@ struct FitOut {
   uint8_t* status;
   uint8_t* iters;
   unsigned long long* evals;  // [3]: reference G-evals, reference T-evals, fused kernel evals (or null)
+  int work_slot;              // g_work slot of this launch (dispatch_fit: round robin)
 };
+
+// Dynamic spot claiming.  Persistent groups take their next spot from a launch-
+// wide counter instead of a static stride, so groups whose spots converge fast
+// take more of them and the launch ends with every group busy until the last few
+// spots (a static stride left ~10% of warp slots idle at the tail: v9 profile,
+// warps_active 14.4 of 16).  g_work[slot] = {next spot, CTAs finished}; the last
+// CTA of a launch resets its slot, so a slot is zero whenever no launch holds it.
+constexpr int kWorkSlots = 256;
+static __device__ unsigned long long g_work[kWorkSlots][2];
 
 // Per-spot LM state, replicated in every lane of the group.  The normal system
 // at `best` (needed again only for lambda retries) lives in the group's shared
@@ -295,7 +305,24 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
     }
     cp_async_commit();
   };
-  prefetch(L.gid);
+  unsigned long long* wk = g_work[out.work_slot];
+  __shared__ unsigned long long claim_bc;  // multi-warp groups: the claimed index, CTA-wide
+  // next spot for the group (want: group-uniform); every lane of the warp (CTA) calls it
+  auto claim = [&](bool want) -> int64_t {
+    if constexpr (SLOTS >= 8) {
+      if (threadIdx.x == 0 && want) claim_bc = atomicAdd(wk, 1ull);
+      __syncthreads();
+      const unsigned long long v = claim_bc;
+      __syncthreads();
+      return (int64_t)v;
+    } else {
+      unsigned long long v = 0ull;
+      if (want && L.gl == 0) v = atomicAdd(wk, 1ull);
+      return (int64_t)__shfl_sync(kFull, v, (threadIdx.x & 31) & ~(8 * SLOTS - 1));
+    }
+  };
+  int64_t nspot = claim(true);  // claimed and staged
+  prefetch(nspot);
 
 #pragma unroll 1
   for (;;) {
@@ -306,7 +333,7 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
     if (__any_sync(kFull, need)) {
       // ---- refill: next spot for every group whose fit finished
       if (need) {
-        spot += L.ngroups;
+        spot = nspot;
         exhausted = spot >= count;
       }
       const bool load = need && !exhausted;
@@ -339,7 +366,11 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
       const double gsum =
           load_spot<P, SLOTS>(S, S.stage + gib * S.sw + nsh, load, L.own, L.base, L.tbase, L.ch, L.tl, sgt, sg40);
       group_sync<SLOTS>();  // the staging window has been read: refill it
-      if (load) prefetch(spot + L.ngroups);
+      const int64_t nxt_spot = claim(load);
+      if (load) {
+        nspot = nxt_spot;
+        prefetch(nspot);
+      }
       const bool gbad = bad || !isfinite(gsum);
       if (load) {
         lane_gt = sgt;
@@ -370,6 +401,15 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
     if (!exhausted && !skip) {
       n_e += 1;
       if (lm_step<P>(s, E, cfg, out, spot, leader, N, n_g, n_t)) need = true;
+    }
+  }
+  // release the claim counter: the last CTA to finish resets the slot
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(wk + 1, 1ull) == (unsigned long long)gridDim.x - 1ull) {
+      wk[0] = 0ull;
+      wk[1] = 0ull;
     }
   }
   if (out.evals != nullptr && leader) {

@@ -130,6 +130,19 @@ __global__ void npexp_kernel(const float* __restrict__ x, float* __restrict__ y,
   if (i < n) y[i] = variant == 0 ? npexp(x[i]) : npexp_ieee_div(x[i]);
 }
 
+// Shared-divisor f64 division check: out = ddiv_with(a, b, ddiv_rcp(b)) (should equal a / b).
+__global__ void ddiv_kernel(const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ out,
+                            int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = ddiv_with(a[i], b[i], ddiv_rcp(b[i]));
+}
+
+cudaError_t launch_ddiv(const double* a, const double* b, double* out, int64_t n, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  ddiv_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(a, b, out, n);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_npexp(const float* x, float* y, int64_t n, int variant, cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
   const int64_t threads = variant == 2 ? (n + 1) / 2 : n;

@@ -61,6 +61,9 @@ cudaError_t launch_simulate(const sf_sim_config& c, int W, int H, int64_t first,
 // u16 -> f32 widening of a streamed chunk (sf_init.cu; sf_fit_batch_u16)
 cudaError_t launch_widen_u16(const uint16_t* in, float* out, int64_t n, cudaStream_t stream);
 
+// shared-divisor f64 division check (sf_init.cu)
+cudaError_t launch_ddiv(const double* a, const double* b, double* out, int64_t n, cudaStream_t stream);
+
 // exhaustive-check helper (sf_init.cu)
 cudaError_t launch_npexp(const float* x, float* y, int64_t n, int variant, cudaStream_t stream);
 
