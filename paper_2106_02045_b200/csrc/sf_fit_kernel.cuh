@@ -44,7 +44,11 @@ struct LMState {
   double* sys;    // [T + P]: JtJ (upper packed) then rhs at best
   float chib, ab, bb;  // chi^2, alpha, beta at best
   int it;
-  bool trial, first, small;
+  unsigned fl;  // kTrial | kFirst | kSmall (one register, no byte packing)
+  static constexpr unsigned kTrial = 1u, kFirst = 2u, kSmall = 4u;
+  __device__ __forceinline__ bool trial() const { return fl & kTrial; }
+  __device__ __forceinline__ bool first() const { return fl & kFirst; }
+  __device__ __forceinline__ bool small() const { return fl & kSmall; }
   int tb;           // first lane of the group's team in this warp (lane-split divisions)
   unsigned tmask;   // the team's lanes
 };
@@ -78,8 +82,8 @@ __device__ __forceinline__ void write_result(const FitOut& o, int64_t spot, bool
 constexpr int kRetry = -1, kAccept = -2;
 template <int P>
 __device__ __forceinline__ int post_trial(LMState<P>& s, const Cfg& c, float chit, bool small, bool* at_best) {
-  if (s.first) {
-    s.first = false;
+  if (s.first()) {
+    s.fl &= ~LMState<P>::kFirst;
     if (s.chib > chit) s.lam = s.lam / c.lam_down;
   }
   if (!small && s.chib < chit && s.lam < c.lam_max) {
@@ -113,12 +117,12 @@ __device__ __forceinline__ bool lm_step(LMState<P>& s, const Eval<P>& E, const C
   constexpr int T = P * (P + 1) / 2;
   int status = -1;       // StopReason | flags once the fit has finished
   bool at_best = false;  // result is the saved best point (restore) rather than E's point
-  bool g_eval = !s.trial;
-  if (s.trial) {
+  bool g_eval = !s.trial();
+  if (s.trial()) {
     const float chit = E.singular ? __int_as_float(0x7fc00000) : E.chi;
-    const int d = post_trial<P>(s, c, chit, s.small, &at_best);
+    const int d = post_trial<P>(s, c, chit, s.small(), &at_best);
     if (d == kAccept) {
-      s.trial = false;  // accepted, budget left: E is exactly the next iteration's G-eval at s.p
+      s.fl &= ~LMState<P>::kTrial;  // accepted, budget left: E is exactly the next iteration's G-eval at s.p
       g_eval = true;
     } else if (d >= 0) {
       status = d;
@@ -142,7 +146,7 @@ __device__ __forceinline__ bool lm_step(LMState<P>& s, const Eval<P>& E, const C
       }
 #pragma unroll
       for (int m = 0; m < T; ++m) s.sys[m] = E.jtj[m];
-      s.first = true;
+      s.fl |= LMState<P>::kFirst;
     }
   }
   // PAPER.md:147-151 and the retry body 159-164
@@ -173,8 +177,7 @@ __device__ __forceinline__ bool lm_step(LMState<P>& s, const Eval<P>& E, const C
         small = small && (fabs(delta[k]) < thr);
       }
       limit_params<P>(c, v, s.p);
-      s.small = small;
-      s.trial = true;
+      s.fl = (s.fl & ~LMState<P>::kSmall) | LMState<P>::kTrial | (small ? LMState<P>::kSmall : 0u);
       n_t += 1;
       return false;  // evaluate the trial point next
     }
@@ -352,9 +355,7 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
         limit_params<P>(cfg, v, s.p);  // SPEC.md:211 "sigma within bounds after limit"
         s.lam = cfg.lam0;
         s.it = 0;
-        s.trial = false;
-        s.first = false;
-        s.small = false;
+        s.fl = 0u;
         if (bad) {  // keep the raw init for the InvalidInput result (oracle/lm.py:fit_single)
 #pragma unroll
           for (int k = 0; k < P; ++k) s.p[k] = init[k];
