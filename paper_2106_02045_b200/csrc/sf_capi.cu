@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -280,20 +281,41 @@ int run_shard(int dev, HostJob& j) {
   sf::build_geom(j.W, j.H, P, geom);
   sf::Cfg kc;
   if (make_cfg(j.cfg, j.W, j.H, kc) != 0) return -1;
-  // chunking: >= 8 chunks for overlap when the shard is large, bounded buffers
-  int64_t chunk = std::max<int64_t>(16384, (total + 7) / 8);
-  chunk = std::min<int64_t>(chunk, std::max<int64_t>(16384, (int64_t)(96 << 20) / (4 * N)));
-  chunk = std::min<int64_t>(chunk, total);
+  // Chunk schedule.  The host path is bound by the H2D copy engine (PCIe Gen5 x16: 53 GB/s at
+  // 100 MB copies, 55.5 GB/s at 900 MB; tools/h2d_bw.py), so copies are large (<= 256 MB), and
+  // the tail halves down to kMinChunk so that the kernel + D2H of the last chunk, which run
+  // after the final H2D, are short.  Three streams overlap H2D(k+1) with kernel(k).
+  const size_t px_bytes_in = j.images16 ? sizeof(uint16_t) : sizeof(float);
+  const int64_t kMinChunk = 16384;
+  // chunk caps (MB of input per H2D), measured with tools/e2e_sweep.py on a B200 (PCIe Gen5 x16):
+  // f32 input is copy-bound and flat above ~64 MB (96 MB best); u16 input is kernel-bound and
+  // wants short chunks so that the first kernel starts early.  SPOTFIT_CHUNK_MB[16] override.
+  auto env_mb = [](const char* name, int64_t dflt) {
+    const char* e = std::getenv(name);
+    const long v = e ? std::strtol(e, nullptr, 10) : 0;
+    return (int64_t)(v > 0 ? v : dflt);
+  };
+  static const int64_t mb32 = env_mb("SPOTFIT_CHUNK_MB", 96), mb16 = env_mb("SPOTFIT_CHUNK_MB16", 24);
+  const int64_t chunk_mb = j.images16 ? mb16 : mb32;
+  const int64_t cap = std::max<int64_t>(kMinChunk, (chunk_mb << 20) / (int64_t)(px_bytes_in * N));
+  const int64_t big = std::min<int64_t>(cap, std::max<int64_t>(kMinChunk, (total + 3) / 4));
+  std::vector<std::pair<int64_t, int64_t>> chunks;  // (offset, spots)
+  for (int64_t lo = 0; lo < total;) {
+    const int64_t rem = total - lo;
+    int64_t n = rem > 2 * big ? big : (rem <= 2 * kMinChunk ? rem : std::max<int64_t>(kMinChunk, rem / 2));
+    chunks.emplace_back(lo, n);
+    lo += n;
+  }
+  int64_t chunk = 0;
+  for (const auto& ch : chunks) chunk = std::max(chunk, ch.second);
   const bool staging = !(j.pinned_in && j.pinned_out);
   if (ensure_ctx(*c, dev, (size_t)chunk, N, P, staging) != 0) return -1;
   SF_CUDA(cudaMemsetAsync(c->d_evals, 0, 3 * sizeof(unsigned long long), c->slot[0].stream));
   SF_CUDA(cudaStreamSynchronize(c->slot[0].stream));
-  std::vector<int64_t> chunk_lo;
-  for (int64_t lo = 0; lo < total; lo += chunk) chunk_lo.push_back(lo);
-  for (size_t ci = 0; ci < chunk_lo.size(); ++ci) {
+  for (size_t ci = 0; ci < chunks.size(); ++ci) {
     Slot& s = c->slot[ci % kStreams];
-    const int64_t lo = j.lo + chunk_lo[ci];
-    const int64_t n = std::min<int64_t>(chunk, total - chunk_lo[ci]);
+    const int64_t lo = j.lo + chunks[ci].first;
+    const int64_t n = chunks[ci].second;
     if (staging) {  // the slot's previous chunk must be finished before its staging is reused
       SF_CUDA(cudaEventSynchronize(s.ev[3]));
       copy_out_staged(s, j);
@@ -350,11 +372,6 @@ int run_shard(int dev, HostJob& j) {
     }
     SF_CUDA(cudaEventRecord(s.ev[3], s.stream));
     ++j.chunks;
-    // per-chunk device times (informational; chunks overlap across streams)
-    if (ci + 1 >= (size_t)kStreams) {
-      Slot& old = c->slot[(ci + 1) % kStreams];
-      (void)old;
-    }
   }
   for (auto& s : c->slot) {
     SF_CUDA(cudaStreamSynchronize(s.stream));
