@@ -435,12 +435,14 @@ def run_ours(args):
     # widenings of the signed addends (non-negative ones take IMAD.WIDE) + 1 MUFU.RCP of the exp
     xu_per_pix = {3: 6 + 6 + 1, 4: 6 + 10 + 1, 5: 21 + 1}[model]
     xu_ops = N * n_k * xu_per_pix
+    inst_per_fit = None  # warp instructions per fit from the committed ncu capture (profiles/ncu_traffic.json)
     traffic = None  # DRAM bytes per launch from the committed ncu capture of this kernel (profiles/)
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             t = json.load(f)
         if model == 3 and (W, H) == (15, 15):
             traffic = t["bytes_per_spot"] * count
+            inst_per_fit = t.get("inst_per_spot")
     except (OSError, KeyError, ValueError):
         pass
     if rank == 0:
@@ -464,6 +466,12 @@ def run_ours(args):
                          "hbm": {"achieved": hbm_bytes / launch_s / 1e9, "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
                                  "frac": (hbm_bytes / launch_s / 1e9) / peaks["hbm_gbs"] if peaks.get("hbm_gbs") else None,
                                  "peak_source": "MEASURED_PEAKS.json (measured)"},
+                         "issue": None if inst_per_fit is None else {
+                             "achieved": inst_per_fit * count / launch_s / 1e12, "peak": sms * 4 * sm_max * 1e6 / 1e12,
+                             "unit": "Twarp-inst/s",
+                             "frac": inst_per_fit * count / launch_s / (sms * 4 * sm_max * 1e6),
+                             "def": "binding resource: warp instructions issued (ncu smsp__inst_executed per fit, "
+                                    "profiles/ncu_traffic.json) vs 1 per clock per SM sub-partition"},
                          "xu": {"achieved": xu_ops / launch_s / 1e12, "peak": sms * 16 * sm_max * 1e6 / 1e12,
                                 "frac": (xu_ops / launch_s) / (sms * 16 * sm_max * 1e6),
                                 "def": "XU pipe (16/clk/SM, measured): F2F.F64.F32 widenings of the signed f64 "
