@@ -56,7 +56,7 @@ struct LMState {
 template <int P>
 __device__ __forceinline__ void write_result(const FitOut& o, int64_t spot, bool leader, const float (&p)[P],
                                              bool singular, float chi, float a, float b, int n_pix, int status,
-                                             int it) {
+                                             int it, double rcp_n5) {
   if (!leader) return;
 #pragma unroll
   for (int k = 0; k < P; ++k) o.params[spot * P + k] = p[k];
@@ -68,7 +68,7 @@ __device__ __forceinline__ void write_result(const FitOut& o, int64_t spot, bool
     o.alpha[spot] = a;
     o.beta[spot] = b;
     // normalized_chi: chi^2/(N-5) in f64, quantised to f32
-    o.nchi2[spot] = n_pix > 5 ? (float)((double)chi / (double)(n_pix - 5)) : chi;
+    o.nchi2[spot] = n_pix > 5 ? (float)ddiv_with((double)chi, (double)(n_pix - 5), rcp_n5) : chi;
   }
   o.status[spot] = (uint8_t)status;
   o.iters[spot] = (uint8_t)it;
@@ -81,10 +81,11 @@ __device__ __forceinline__ void write_result(const FitOut& o, int64_t spot, bool
 // *at_best: restore best).
 constexpr int kRetry = -1, kAccept = -2;
 template <int P>
-__device__ __forceinline__ int post_trial(LMState<P>& s, const Cfg& c, float chit, bool small, bool* at_best) {
+__device__ __forceinline__ int post_trial(LMState<P>& s, const Cfg& c, float chit, bool small, bool* at_best,
+                                          double rcp_down) {
   if (s.first()) {
     s.fl &= ~LMState<P>::kFirst;
-    if (s.chib > chit) s.lam = s.lam / c.lam_down;
+    if (s.chib > chit) s.lam = ddiv_with(s.lam, c.lam_down, rcp_down);  // == s.lam / c.lam_down
   }
   if (!small && s.chib < chit && s.lam < c.lam_max) {
     s.lam = s.lam * c.lam_up;
@@ -99,7 +100,7 @@ __device__ __forceinline__ int post_trial(LMState<P>& s, const Cfg& c, float chi
     return SF_STOP_MIN_DELTA | SF_FLAG_NOIMP;
   }
   if ((double)chit < c.max_error) return SF_STOP_MAX_ERROR;
-  if ((double)s.chib * (1.0 - c.min_delta) < (double)chit) return SF_STOP_MIN_DELTA;
+  if ((double)s.chib * c.one_minus_min_delta < (double)chit) return SF_STOP_MIN_DELTA;
   if (small) return SF_STOP_MIN_STEP;
   if (s.it >= c.max_it) return SF_STOP_MAX_ITERATIONS;
   return kAccept;
@@ -113,14 +114,15 @@ __device__ __forceinline__ int post_trial(LMState<P>& s, const Cfg& c, float chi
 // warp executes it once per trip instead of once per divergent path.
 template <int P>
 __device__ __forceinline__ bool lm_step(LMState<P>& s, const Eval<P>& E, const Cfg& c, const FitOut& o,
-                                        int64_t spot, bool leader, int n_pix, unsigned& n_g, unsigned& n_t) {
+                                        int64_t spot, bool leader, int n_pix, unsigned& n_g, unsigned& n_t,
+                                        const double* kc) {
   constexpr int T = P * (P + 1) / 2;
   int status = -1;       // StopReason | flags once the fit has finished
   bool at_best = false;  // result is the saved best point (restore) rather than E's point
   bool g_eval = !s.trial();
   if (s.trial()) {
     const float chit = E.singular ? __int_as_float(0x7fc00000) : E.chi;
-    const int d = post_trial<P>(s, c, chit, s.small(), &at_best);
+    const int d = post_trial<P>(s, c, chit, s.small(), &at_best, kc[0]);
     if (d == kAccept) {
       s.fl &= ~LMState<P>::kTrial;  // accepted, budget left: E is exactly the next iteration's G-eval at s.p
       g_eval = true;
@@ -173,7 +175,8 @@ __device__ __forceinline__ bool lm_step(LMState<P>& s, const Eval<P>& E, const C
 #pragma unroll
       for (int k = 0; k < P; ++k) {
         v[k] = (double)s.best[k] + delta[k];
-        const double thr = c.min_step * fmax(fabs((double)s.best[k]), 1.0);
+        // min_step * max(|best|, 1) (oracle/lm.py): the max of two f32 values is exact in f32
+        const double thr = c.min_step * (double)fmaxf(fabsf(s.best[k]), 1.0f);
         small = small && (fabs(delta[k]) < thr);
       }
       limit_params<P>(c, v, s.p);
@@ -182,14 +185,14 @@ __device__ __forceinline__ bool lm_step(LMState<P>& s, const Eval<P>& E, const C
       return false;  // evaluate the trial point next
     }
     // StepFailed: chi'^2 = +inf, not small -> retry with a raised lambda or stop
-    const int d = post_trial<P>(s, c, __int_as_float(0x7f800000), false, &at_best);
+    const int d = post_trial<P>(s, c, __int_as_float(0x7f800000), false, &at_best, kc[0]);
     if (d >= 0) status = d;  // (never kAccept: +inf is not below chi_best)
   }
   float rp[P];
 #pragma unroll
   for (int k = 0; k < P; ++k) rp[k] = at_best ? s.best[k] : s.p[k];
   write_result<P>(o, spot, leader, rp, !at_best && E.singular, at_best ? s.chib : E.chi, at_best ? s.ab : E.alpha,
-                  at_best ? s.bb : E.beta, n_pix, status, s.it);
+                  at_best ? s.bb : E.beta, n_pix, status, s.it, kc[1]);
   return true;
 }
 
@@ -212,7 +215,7 @@ struct LaneSetup {
     return owns(own, j) ? (j < ch ? base + 8 * j : tbase + (j - ch)) : -1;
   }
 
-  __device__ __forceinline__ void init(Smem<P, SLOTS>& S, const Geom& geom) {
+  __device__ __forceinline__ void init(Smem<P, SLOTS>& S, const Geom& geom, double cfg_lam_down = 1.0) {
     constexpr int LANES = 8 * SLOTS;
     const int lane = threadIdx.x & 31;
     if constexpr (SLOTS >= 8) {
@@ -255,6 +258,11 @@ struct LaneSetup {
       }
       for (int j = ch & ~1; j < ch + tl; ++j) S.so[j - (ch & ~1)].xy[SLOTS >= 8 ? 0 : gl] = xy(j);
     }
+    // CTA constants: reciprocal stages of the fixed divisors lambda_down and N - 5
+    if (threadIdx.x == 0) {
+      S.kc[0] = ddiv_rcp(cfg_lam_down);
+      S.kc[1] = ddiv_rcp((double)(geom.N - 5));
+    }
     // pixel values start at 0 (load_spot rewrites a group's slots on every refill)
     for (int i = 0; i < ch / 2; ++i) S.pr[i].g[threadIdx.x] = make_float2(0.0f, 0.0f);
     for (int r = 0; r < (ch & 1) + tl; ++r) S.so[r].g[threadIdx.x] = 0.0f;
@@ -273,7 +281,7 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
   Smem<P, SLOTS> S;
   S.bind(smem_raw, geom.ch, geom.tl, geom.N);
   LaneSetup<P, SLOTS> L;
-  L.init(S, geom);
+  L.init(S, geom, cfg.lam_down);
   const bool leader = L.gl == 0;
   const int N = geom.N;
   const double n = (double)N;
@@ -381,7 +389,8 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
       if (load) {
         G = gsum;
         if (gbad) {
-          write_result<P>(out, spot, leader, s.p, true, 0.f, 0.f, 0.f, N, SF_STOP_NOT_CONVERGED | SF_FLAG_INVALID, 0);
+          write_result<P>(out, spot, leader, s.p, true, 0.f, 0.f, 0.f, N, SF_STOP_NOT_CONVERGED | SF_FLAG_INVALID, 0,
+                          S.kc[1]);
           need = true;  // fetch the next spot on the next trip
           skip = true;
         } else {
@@ -401,7 +410,7 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
     }
     if (!exhausted && !skip) {
       n_e += 1;
-      if (lm_step<P>(s, E, cfg, out, spot, leader, N, n_g, n_t)) need = true;
+      if (lm_step<P>(s, E, cfg, out, spot, leader, N, n_g, n_t, S.kc)) need = true;
     }
   }
   // release the claim counter: the last CTA to finish resets the slot
