@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
       // f32 values cannot overflow f64), so it doubles as the InvalidInput pixel check
       bool sgt, sg40;
       const double gsum =
-          load_spot<P, SLOTS>(S, S.stage + gib * S.sw + nsh, load, L.own, L.base, L.tbase, L.ch, L.tl, sgt, sg40);
+          load_spot<P, SLOTS, FULL>(S, S.stage + gib * S.sw + nsh, load, L.own, L.base, L.tbase, L.ch, L.tl, sgt, sg40);
       group_sync<SLOTS>();  // the staging window has been read: refill it
       const int64_t nxt_spot = claim(load);
       if (load) {
