@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
 
     Eval<P> E;
     if constexpr (P == 5) {
-      evaluate_explicit5<SLOTS>(S, L.lg, L.own, L.ch, L.tl, s.p, E);
+      evaluate_explicit5<SLOTS, FULL>(S, L.lg, L.own, L.ch, L.tl, s.p, lane_g40, !exhausted && !skip, E);
     } else {
       evaluate<P, SLOTS, FULL>(S, L.lg, L.own, L.ch, L.tl, G, n, s.p, warp_gt, lane_g40, !exhausted && !skip, E);
     }

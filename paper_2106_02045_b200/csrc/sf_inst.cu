@@ -14,8 +14,7 @@
 namespace sf {
 
 int SF_UNIT_NAME(launch_fit, SF_P, SF_SLOTS)(const LaunchFit& a, cudaError_t* err) {
-  // FULL (no chain masking) only matters to the implicit models' packed chain loops
-  auto kern = (SF_P != 5 && a.geom.full) ? fit_kernel<SF_P, SF_SLOTS, SF_P != 5> : fit_kernel<SF_P, SF_SLOTS, false>;
+  auto kern = a.geom.full ? fit_kernel<SF_P, SF_SLOTS, true> : fit_kernel<SF_P, SF_SLOTS, false>;
   constexpr int tpb = threads_per_block<SF_SLOTS>();
   constexpr int groups_per_block = SF_SLOTS >= 8 ? 1 : (tpb / 32) * (32 / (8 * SF_SLOTS));
   const size_t smem = Smem<SF_P, SF_SLOTS>::bytes(a.geom.ch, a.geom.tl, a.geom.N);

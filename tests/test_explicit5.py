@@ -87,3 +87,28 @@ def test_gpu_explicit5_matches_oracle(oracle_lib, W, H):
         assert bits_equal(np.asarray(getattr(res, k)), np.asarray(ref[k])), (W, H, k)
     auto = sf.fit_batch(im.reshape(count, H, W), engine="explicit5")  # GPU initializer incl. alpha, beta
     assert bits_equal(auto.params, res.params)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("W,H", [(15, 15), (17, 15)])
+def test_gpu_explicit5_untamed_inputs_match_oracle(oracle_lib, W, H):
+    """Explicit-5 outside the integer-widening fast path (negative, -0, > 2^40 and
+    tiny pixel values, mixed within warps) matches the oracle bit for bit."""
+    import paper_2106_02045_b200 as sf
+
+    count = 2400
+    im, _ = sf.simulate_batch(sf.SimConfig(width=W, height=H, count=count, seed=W * 7 + H))
+    im = im.reshape(count, -1).copy()
+    k = np.arange(count) % 6
+    im[k == 1] -= np.float32(45.0)
+    z = im[k == 2]
+    z[:, ::5] = np.float32(-0.0)
+    im[k == 2] = z
+    im[k == 3] *= np.float32(1e12)
+    im[k == 4] *= np.float32(3e-30)
+    ini3, amps = oinit.estimate_initial_batch(im, W, H, 0.3, float(max(W, H)))
+    ini5 = np.concatenate([ini3, amps], axis=1).astype(np.float32)
+    res = sf.fit_batch(im, ini5, grid=sf.PixelGrid(W, H), engine="explicit5")
+    ref = oracle_lib.fit_batch(im, ini5, W, H, lm.LMConfig.for_grid(W, H))
+    for key in FIELDS:
+        assert bits_equal(np.asarray(getattr(res, key)), np.asarray(ref[key])), (W, H, key)
