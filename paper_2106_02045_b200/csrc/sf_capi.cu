@@ -61,6 +61,7 @@ int make_cfg(const sf_config* c, int W, int H, sf::Cfg& k) {
   k.max_error = c->max_error;
   k.min_delta = c->min_delta;
   k.one_minus_min_delta = 1.0 - c->min_delta;
+  k.zero = 0.0;
   k.min_step = c->min_step;
   k.lam0 = c->lambda_init;
   k.lam_up = c->lambda_up;

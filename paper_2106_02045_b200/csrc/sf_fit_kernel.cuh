@@ -168,6 +168,15 @@ __device__ __forceinline__ bool lm_step(LMState<P>& s, const Eval<P>& E, const C
 #else
       solved = solve_step<P>(jtj, rhs, s.lam, delta);
 #endif
+#ifdef SF_ABL_SOLVE2
+      {  // ablation: a second solve at a perturbed lambda (marginal cost of the damped solve)
+        double d2[P];
+        const bool ok2 = solve_step<P>(jtj, rhs, s.lam + c.zero * s.lam, d2);
+#pragma unroll
+        for (int k = 0; k < P; ++k) delta[k] = __fma_rn(d2[k], c.zero, delta[k]);
+        solved = solved && (ok2 || c.zero == 0.0);
+      }
+#endif
     }
     if (solved) {
       double v[P];
@@ -406,7 +415,8 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
     if constexpr (P == 5) {
       evaluate_explicit5<SLOTS, FULL>(S, L.lg, L.own, L.ch, L.tl, s.p, lane_g40, !exhausted && !skip, E);
     } else {
-      evaluate<P, SLOTS, FULL>(S, L.lg, L.own, L.ch, L.tl, G, n, s.p, warp_gt, lane_g40, !exhausted && !skip, E);
+      evaluate<P, SLOTS, FULL>(S, L.lg, L.own, L.ch, L.tl, G, n, s.p, warp_gt, lane_g40, !exhausted && !skip, E,
+                               nullptr, cfg.zero);
     }
     if (!exhausted && !skip) {
       n_e += 1;
