@@ -153,12 +153,21 @@ __device__ __forceinline__ bool lm_step(LMState<P>& s, const Eval<P>& E, const C
   }
   // PAPER.md:147-151 and the retry body 159-164
 #pragma unroll 1
+  bool from_regs = SF_SOLVE_FROMREGS && g_eval;  // first solve after a G-eval: the system straight from E
   while (status < 0) {
     double jtj[T], rhs[P], delta[P];
+    if (from_regs) {
 #pragma unroll
-    for (int m = 0; m < T; ++m) jtj[m] = s.sys[m];
+      for (int m = 0; m < T; ++m) jtj[m] = E.jtj[m];
 #pragma unroll
-    for (int k = 0; k < P; ++k) rhs[k] = s.sys[T + k];
+      for (int k = 0; k < P; ++k) rhs[k] = E.rhs[k];
+    } else {  // lambda retries re-solve the system saved at best
+#pragma unroll
+      for (int m = 0; m < T; ++m) jtj[m] = s.sys[m];
+#pragma unroll
+      for (int k = 0; k < P; ++k) rhs[k] = s.sys[T + k];
+    }
+    from_regs = false;
     bool solved;
     if constexpr (P == 5) {
       solved = solve_pivot5(jtj, rhs, s.lam, delta);
