@@ -96,6 +96,10 @@ def lib():
         _lib.npexp_f32.restype = ctypes.c_float
         _lib.npexp_f32.argtypes = [ctypes.c_float]
         _lib.npexp_f32_array.argtypes = [f32p, f32p, ctypes.c_int64]
+        _lib.npexp_f32_clamped.restype = ctypes.c_float
+        _lib.npexp_f32_clamped.argtypes = [ctypes.c_float]
+        _lib.npexp_clamp_mismatches.restype = ctypes.c_int64
+        _lib.npexp_clamp_mismatches.argtypes = [ctypes.c_float, ctypes.c_float]
         _lib.pw_sum.restype = ctypes.c_double
         _lib.pw_sum.argtypes = [f32p, ctypes.c_int]
         _lib.sf_oracle_solve.restype = ctypes.c_int

@@ -56,6 +56,41 @@ static float ldexp_single_round(float r, int q) {
   }
 }
 
+/* The fit kernel's packed exp (sf_device.cuh:npexp2) drops the underflow guard and clamps
+ * the argument instead: max.NaN(x, -104) followed by the unguarded formula.  This restates
+ * that form; npexp_clamp_mismatches() counts the float32 x in [lo, hi] where it differs from
+ * npexp_f32 (tests/test_oracle_numerics.py: must be none on the kernel's domain x <= 0). */
+float npexp_f32_clamped(float x) {
+  if (x != x) return x;
+  if (x < -104.0f) x = -104.0f;
+  volatile float t = x * 1.442695040888963407359924681001892137f;
+  float q = (t + 0x1.8p23f) - 0x1.8p23f;
+  float y = fmaf(q, -6.93145752e-1f, x);
+  y = fmaf(q, -1.42860677e-6f, y);
+  float n = fmaf(5.082762527590693718096e-4f, y, 6.757896990527504603057e-3f);
+  n = fmaf(n, y, 5.114512081637298353406e-2f);
+  n = fmaf(n, y, 2.473615434895520810817e-1f);
+  n = fmaf(n, y, 7.257664613233124478488e-1f);
+  n = fmaf(n, y, 9.999999999980870924916e-1f);
+  float d = fmaf(2.159509375685829852307e-2f, y, -2.742335390411667452936e-1f);
+  d = fmaf(d, y, 1.0f);
+  float r = n / d;
+  return ldexp_single_round(r, (int)q);
+}
+
+int64_t npexp_clamp_mismatches(float lo, float hi) {
+  int64_t bad = 0;
+  for (float x = lo; x <= hi; x = nextafterf(x, INFINITY)) {
+    const float a = npexp_f32(x), b = npexp_f32_clamped(x);
+    uint32_t ua, ub;
+    memcpy(&ua, &a, 4);
+    memcpy(&ub, &b, 4);
+    bad += ua != ub;
+    if (x == hi) break;
+  }
+  return bad;
+}
+
 float npexp_f32(float x) {
   if (x != x) return x;
   if (x >= 88.72283935546875f) return INFINITY;

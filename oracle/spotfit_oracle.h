@@ -42,6 +42,8 @@ typedef struct {
 } sf_oracle_result_t;
 
 float npexp_f32(float x);
+float npexp_f32_clamped(float x);
+int64_t npexp_clamp_mismatches(float lo, float hi);
 void npexp_f32_array(const float* x, float* y, int64_t n);
 double pw_sum(const float* a, int n);
 int sf_oracle_eval(const float* g, int W, int H, int P, const float* p, sf_oracle_eval_t* e);

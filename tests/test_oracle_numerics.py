@@ -43,3 +43,15 @@ def test_pairwise_sum_matches_live_numpy(oracle_lib):
     for n in list(range(1, 260)) + [441, 511, 512, 513, 1000, 1023, 1024]:
         x = (rng.standard_normal(n) * 10.0 ** rng.uniform(-4, 4, n)).astype(np.float32)
         assert oracle_lib.pw_sum(x) == x.sum(dtype=np.float64)
+
+
+def test_exp_underflow_clamp_equals_guard():
+    """The kernel's packed exp replaces numpy's underflow guard (x <= -103.97208 -> +0) by
+    clamping x at -104 (sf_device.cuh:npexp2).  Equal bit for bit on every float32 in
+    [-200, -100] (the guard region and far below it) and on the clamp value itself."""
+    from oracle import oracle_c
+
+    lib = oracle_c.lib()
+    assert lib.npexp_clamp_mismatches(-200.0, -100.0) == 0
+    for x in (-1e30, -3.4e38, -104.0, -103.97208404541015625):
+        assert lib.npexp_f32_clamped(x) == 0.0 and lib.npexp_f32(x) == 0.0
