@@ -18,56 +18,79 @@ namespace {
 constexpr double kExpMinusHalf = 0x1.368b2fc6f960ap-1;  // exp(-0.5), correctly rounded
 constexpr double kPi = 3.141592653589793115997963468544185161590576171875;
 
-__global__ void __launch_bounds__(256) init_kernel(const float* __restrict__ images, int W, int H, int64_t count,
-                                                   int P, double smin, double smax, float* __restrict__ inits,
-                                                   float* __restrict__ amps) {
-  const int64_t spot = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+// One warp per spot; the spot is staged in shared memory with coalesced loads (the 3x3 means
+// read it 9x), and pixel coordinates come from the exact float reciprocal (idx + 0.5) / W
+// instead of integer division.  Arithmetic exactly as pinned above.
+constexpr int kInitWarps = 8;
+__global__ void __launch_bounds__(32 * kInitWarps) init_kernel(const float* __restrict__ images, int W, int H,
+                                                              int64_t count, int P, double smin, double smax,
+                                                              float* __restrict__ inits, float* __restrict__ amps) {
+  extern __shared__ float init_smem[];  // [kInitWarps][N]
+  const int warp = threadIdx.x >> 5;
+  const int64_t spot = (int64_t)blockIdx.x * kInitWarps + warp;
   const int lane = threadIdx.x & 31;
   if (spot >= count) return;
   const int N = W * H;
+  float* sg = init_smem + warp * N;
   const float* g = images + spot * (int64_t)N;
+  for (int i = lane; i < N; i += 32) sg[i] = __ldg(g + i);
+  __syncwarp();
+  const float Wf = (float)W, invW = 1.0f / Wf;
   float best = -INFINITY, lo = INFINITY;
   int bidx = INT_MAX;
   for (int i = lane; i < N; i += 32) {
-    const int x = i % W, y = i / W;
+    // y = floor((i + 0.5) / W) exactly (small integers, never a tie), x = i - y W
+    const int y = (int)(((float)i + 0.5f) * invW);
+    const int x = i - y * W;
     double s = 0.0;
     int cnt = 0;
+#pragma unroll
     for (int dy = -1; dy <= 1; ++dy) {
       const int yy = y + dy;
-      if (yy < 0 || yy >= H) continue;
+      const bool vy = yy >= 0 && yy < H;
+#pragma unroll
       for (int dx = -1; dx <= 1; ++dx) {
         const int xx = x + dx;
-        if (xx < 0 || xx >= W) continue;
-        s = s + (double)__ldg(g + yy * W + xx);
-        ++cnt;
+        const bool v = vy && xx >= 0 && xx < W;
+        const float val = v ? sg[yy * W + xx] : 0.0f;
+        if (v) {
+          s = s + (double)val;
+          ++cnt;
+        }
       }
     }
     const float v = (float)(s / (double)cnt);
-    if (v > best || (v == best && i < bidx)) { best = v; bidx = i; }
+    if (v > best || (v == best && i < bidx)) {
+      best = v;
+      bidx = i;
+    }
     lo = fminf(lo, v);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const float ob = __shfl_xor_sync(0xffffffffu, best, o);
     const int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
-    if (ob > best || (ob == best && oi < bidx)) { best = ob; bidx = oi; }
+    if (ob > best || (ob == best && oi < bidx)) {
+      best = ob;
+      bidx = oi;
+    }
     lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
   }
   if (bidx == INT_MAX) bidx = 0;
   const float alpha = (float)((double)best - (double)lo);
   const double thr = (double)alpha * kExpMinusHalf + (double)lo;
   int m = 0;
-  for (int i = lane; i < N; i += 32) m += ((double)__ldg(g + i) > thr) ? 1 : 0;
+  for (int i = lane; i < N; i += 32) m += ((double)sg[i] > thr) ? 1 : 0;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
-  double sg = sqrt((double)m / kPi);
-  sg = sg < smin ? smin : (sg > smax ? smax : sg);
+  double sgm = sqrt((double)m / kPi);
+  sgm = sgm < smin ? smin : (sgm > smax ? smax : sgm);
   if (lane == 0) {
     float* o = inits + spot * P;
     o[0] = (float)(bidx % W);
     o[1] = (float)(bidx / W);
-    o[2] = (float)sg;
-    if (P == 4) o[3] = (float)sg;
+    o[2] = (float)sgm;
+    if (P == 4) o[3] = (float)sgm;
     if (amps != nullptr) {
       amps[2 * spot] = alpha;
       amps[2 * spot + 1] = lo;
@@ -79,9 +102,10 @@ __global__ void __launch_bounds__(256) init_kernel(const float* __restrict__ ima
 cudaError_t launch_estimate_initial(const float* images, int W, int H, int64_t count, int P, double sigma_min,
                                     double sigma_max, float* inits, float* amps, cudaStream_t stream) {
   if (count <= 0) return cudaSuccess;
-  const int64_t threads = count * 32;
-  const int64_t blocks = (threads + 255) / 256;
-  init_kernel<<<(unsigned)blocks, 256, 0, stream>>>(images, W, H, count, P, sigma_min, sigma_max, inits, amps);
+  const int64_t blocks = (count + kInitWarps - 1) / kInitWarps;
+  const size_t smem = (size_t)kInitWarps * W * H * sizeof(float);  // <= 32 KB (N <= 1024)
+  init_kernel<<<(unsigned)blocks, 32 * kInitWarps, smem, stream>>>(images, W, H, count, P, sigma_min, sigma_max,
+                                                                   inits, amps);
   return cudaGetLastError();
 }
 
