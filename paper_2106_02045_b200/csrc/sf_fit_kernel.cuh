@@ -49,8 +49,6 @@ struct LMState {
   __device__ __forceinline__ bool trial() const { return fl & kTrial; }
   __device__ __forceinline__ bool first() const { return fl & kFirst; }
   __device__ __forceinline__ bool small() const { return fl & kSmall; }
-  int tb;           // first lane of the group's team in this warp (lane-split divisions)
-  unsigned tmask;   // the team's lanes
 };
 
 template <int P>
@@ -153,30 +151,17 @@ __device__ __forceinline__ bool lm_step(LMState<P>& s, const Eval<P>& E, const C
   }
   // PAPER.md:147-151 and the retry body 159-164
 #pragma unroll 1
-  bool from_regs = SF_SOLVE_FROMREGS && g_eval;  // first solve after a G-eval: the system straight from E
   while (status < 0) {
     double jtj[T], rhs[P], delta[P];
-    if (from_regs) {
 #pragma unroll
-      for (int m = 0; m < T; ++m) jtj[m] = E.jtj[m];
+    for (int m = 0; m < T; ++m) jtj[m] = s.sys[m];
 #pragma unroll
-      for (int k = 0; k < P; ++k) rhs[k] = E.rhs[k];
-    } else {  // lambda retries re-solve the system saved at best
-#pragma unroll
-      for (int m = 0; m < T; ++m) jtj[m] = s.sys[m];
-#pragma unroll
-      for (int k = 0; k < P; ++k) rhs[k] = s.sys[T + k];
-    }
-    from_regs = false;
+    for (int k = 0; k < P; ++k) rhs[k] = s.sys[T + k];
     bool solved;
     if constexpr (P == 5) {
       solved = solve_pivot5(jtj, rhs, s.lam, delta);
     } else {
-#if SF_TEAM_SOLVE
-      solved = solve_step_team<P>(jtj, rhs, s.lam, delta, s.tb, s.tmask);
-#else
       solved = solve_step<P>(jtj, rhs, s.lam, delta);
-#endif
 #ifdef SF_ABL_SOLVE2
       {  // ablation: a second solve at a perturbed lambda (marginal cost of the damped solve)
         double d2[P];
@@ -306,13 +291,7 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
 
   double G = 0.0;
   LMState<P> s;
-  {
-    constexpr int LANES = 8 * SLOTS;
-    s.sys = S.sys + L.gib() * Smem<P, SLOTS>::kSysQ;
-    constexpr int TEAM = LANES < 32 ? LANES : 32;
-    s.tb = team_base<SLOTS>();
-    s.tmask = TEAM == 32 ? kFull : ((1u << TEAM) - 1u) << s.tb;
-  }
+  s.sys = S.sys + L.gib() * Smem<P, SLOTS>::kSysQ;
   int64_t spot = L.gid - L.ngroups;
   bool need = true, exhausted = false;
   bool lane_gt = true, lane_g40 = true, warp_gt = true;  // spot tameness (pixel_sum)
