@@ -41,7 +41,9 @@ struct LMState {
   float p[P];     // parameters under evaluation (G point or trial point)
   float best[P];  // PAPER.md:144 "best := current"
   double lam;
-  double* sys;    // [T + P]: JtJ (upper packed) then rhs at best
+  double* sys;    // [T + P]: JtJ (upper packed) then rhs at best (group's copy for this warp)
+  unsigned gmask;  // the group's lanes in this warp; lane gl == 0 of them (sys_writer) stores sys
+  bool sys_writer;
   float chib, ab, bb;  // chi^2, alpha, beta at best
   int it;
   unsigned fl;  // kTrial | kFirst | kSmall (one register, no byte packing)
@@ -140,12 +142,15 @@ __device__ __forceinline__ bool lm_step(LMState<P>& s, const Eval<P>& E, const C
       s.ab = E.alpha;
       s.bb = E.beta;
 #pragma unroll
-      for (int k = 0; k < P; ++k) {
-        s.best[k] = s.p[k];
-        s.sys[T + k] = E.rhs[k];
-      }
+      for (int k = 0; k < P; ++k) s.best[k] = s.p[k];
+      // every lane holds the identical system: one lane per (group, warp) stores it
+      if (s.sys_writer) {
 #pragma unroll
-      for (int m = 0; m < T; ++m) s.sys[m] = E.jtj[m];
+        for (int k = 0; k < P; ++k) s.sys[T + k] = E.rhs[k];
+#pragma unroll
+        for (int m = 0; m < T; ++m) s.sys[m] = E.jtj[m];
+      }
+      __syncwarp(s.gmask);
       s.fl |= LMState<P>::kFirst;
     }
   }
@@ -291,7 +296,12 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
 
   double G = 0.0;
   LMState<P> s;
-  s.sys = S.sys + L.gib() * Smem<P, SLOTS>::kSysQ;
+  s.sys = S.sys + (SLOTS >= 8 ? (int)(threadIdx.x >> 5) : L.gib()) * Smem<P, SLOTS>::kSysQ;
+  {
+    constexpr int LW = 8 * SLOTS < 32 ? 8 * SLOTS : 32;
+    s.gmask = LW == 32 ? kFull : ((1u << LW) - 1u) << ((threadIdx.x & 31) & ~(LW - 1));
+    s.sys_writer = ((threadIdx.x & 31) & (LW - 1)) == 0;
+  }
   int64_t spot = L.gid - L.ngroups;
   bool need = true, exhausted = false;
   bool lane_gt = true, lane_g40 = true, warp_gt = true;  // spot tameness (pixel_sum)

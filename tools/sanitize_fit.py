@@ -1,0 +1,40 @@
+"""Small fits for compute-sanitizer runs (memcheck / racecheck / synccheck): one batch per
+geometry family (warp-shared groups, one-leaf groups, one-warp groups, multi-warp groups,
+ragged trees, explicit-5), results checked against the C oracle."""
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_2106_02045_b200 as sf  # noqa: E402
+from oracle import initializer as oinit  # noqa: E402
+from oracle import lm, oracle_c  # noqa: E402
+
+CASES = [(15, 15, 3, 96), (11, 11, 3, 96), (21, 21, 4, 32), (32, 32, 3, 16), (13, 10, 3, 64), (15, 15, 5, 64),
+         (1, 5, 3, 64)]
+ok = True
+for W, H, model, count in CASES:
+    im, _ = sf.simulate_batch(sf.SimConfig(width=W, height=H, count=count, seed=W * 13 + H, model=min(model, 4)))
+    im = im.reshape(count, -1)
+    ini, amps = oinit.estimate_initial_batch(im, W, H, 0.3, float(max(W, H)), 4 if model == 4 else 3)
+    if model == 5:
+        ini = np.concatenate([ini, amps], axis=1).astype(np.float32)
+    engine = {3: "implicit3", 4: "elliptical", 5: "explicit5"}[model]
+    res = sf.fit_batch(im, ini, grid=sf.PixelGrid(W, H), engine=engine)
+    ref = oracle_c.fit_batch(im, ini, W, H, lm.LMConfig.for_grid(W, H))
+    same = all(np.array_equal(np.asarray(getattr(res, k)).view(np.uint8), np.asarray(ref[k]).view(np.uint8))
+               for k in ("params", "alpha", "beta", "nchi2", "status", "iterations"))
+    ok &= same
+    print(f"{W}x{H} P={model}: {'ok' if same else 'MISMATCH'}", flush=True)
+# the other kernels: GPU initializer, model-level evaluation, device simulator
+import torch  # noqa: E402
+
+for W, H in ((15, 15), (21, 21), (32, 32)):
+    im, tr = sf.simulate_batch(sf.SimConfig(width=W, height=H, count=40, seed=5))
+    ini, _ = sf.estimate_initial_batch(im, 3, grid=sf.PixelGrid(W, H))
+    rec = sf.evaluate_batch(im.reshape(40, -1), tr[:, :3], W, H)
+    dev = sf.simulate_batch_device(sf.SimConfig(width=W, height=H, count=40, seed=5))
+    torch.cuda.synchronize()
+print("SANITIZE_FIT", "ok" if ok else "FAIL")
