@@ -1,12 +1,13 @@
 // sf_fit_kernel.cuh -- the fused, device-resident LM fit kernel (sm_100a).
 //
 // One "group" of 8*SLOTS chain lanes fits one spot at a time; groups are
-// persistent and walk the batch with a static stride (spot = gid, gid+G, ...),
-// so a group that stops early simply loads its next spot while its warp-mates
-// keep iterating.  Each loop trip is: [refill groups that finished] ->
-// one fused evaluation (sf_device.cuh:evaluate) -> the LM state machine of
-// SURVEY App. A, divergent across groups but cheap.  No
-// host round trip happens inside a fit.
+// persistent and claim their next spot from a launch-wide counter (g_work), so
+// a group that stops early loads its next spot while its warp-mates keep
+// iterating, and the launch ends with every group busy.  Each loop trip is:
+// [refill groups that finished] -> one fused evaluation
+// (sf_device.cuh:evaluate) -> the LM state machine of SURVEY App. A
+// (PAPER.md:126-180), divergent across groups but cheap.  No host round trip
+// happens inside a fit.
 #pragma once
 #include "sf_device.cuh"
 
@@ -304,7 +305,7 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
   }
   int64_t spot = L.gid - L.ngroups;
   bool need = true, exhausted = false;
-  bool lane_gt = true, lane_g40 = true, warp_gt = true;  // spot tameness (pixel_sum)
+  bool lane_gt = true, lane_g40 = true, warp_gt = true;  // spot tameness (load_spot)
   unsigned n_g = 0, n_t = 0, n_e = 0;
 
   // Next-spot prefetch: the group streams the next spot into its staging window
