@@ -281,7 +281,7 @@ struct LaneSetup {
 
 template <int P, int SLOTS, bool FULL>
 __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
-                                  P == 5 ? (SLOTS >= 8 ? 1 : 2)
+                                  P == 5 ? (SLOTS >= 8 ? 1 : SF_MINB_P5)
                                          : (SLOTS == 8 ? 2 * SF_MINB_P3 : (SLOTS == 16 ? SF_MINB_P3
                                                                                      : (P == 3 ? SF_MINB_P3 : SF_MINB_P4))))
     fit_kernel(const float* __restrict__ images, const float* __restrict__ inits, int64_t count, const Geom geom,
