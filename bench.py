@@ -48,6 +48,31 @@ OPS_G = {3: 67, 4: 88, 5: 60}  # explicit-5: 39 FP32 + 21 reduction adds per pix
 OPS_T = {3: 18, 4: 18, 5: 60}
 
 
+def host_info() -> dict:
+    """CPU model and numpy's float32 SIMD dispatch (the reference's exp is numpy's SIMD kernel)."""
+    cpu = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    cpu = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    simd = []
+    try:
+        from numpy._core._multiarray_umath import __cpu_features__ as feats  # numpy >= 2
+    except ImportError:  # pragma: no cover
+        try:
+            from numpy.core._multiarray_umath import __cpu_features__ as feats
+        except ImportError:
+            feats = {}
+    for k in ("AVX512_SPR", "AVX512_ICL", "AVX512_SKX", "AVX512F", "AVX2", "FMA3"):
+        if feats.get(k):
+            simd.append(k)
+    return {"cpu": cpu, "numpy": np.__version__, "simd": simd[:3]}
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -176,7 +201,7 @@ def run_reference(args):
         "config": {"workload": f"{args.config}: {W}x{H} {'symmetric' if model == 3 else 'elliptical'}, "
                                f"bounded sample of {sample} spots per step", "spots_per_step": sample,
                    "cores": cores},
-        "cpu_baseline": {"value": value, "unit": "fits/s", "cores": cores, "kind": kind,
+        "cpu_baseline": {"value": value, "unit": "fits/s", "cores": cores, "kind": kind, "host": host_info(),
                          "sample": f"{sample} spots of the {W}x{H} workload per step, {args.steps} steps; "
                                    "arithmetic: reference spotfit.model from baseline/_ref, LM loop oracle/lm.py"},
         "e2e": {"value": value, "unit": "fits/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -412,7 +437,7 @@ def run_ours(args):
         c_v = cpu_c_port(W, H, images, ini, min(count, 20 * samp), cores)
         src = ("the unmodified reference spotfit.model (baseline/_ref)" if kind == "reference"
                else "oracle/model_np.py (restated reference numpy arithmetic)")
-        result["cpu_baseline"] = {"value": cpu_v, "unit": "fits/s", "cores": cores, "kind": kind,
+        result["cpu_baseline"] = {"value": cpu_v, "unit": "fits/s", "cores": cores, "kind": kind, "host": host_info(),
                                   "sample": f"{samp} spots of this workload, LM loop oracle/lm.py over {src}, "
                                             f"{cpu_dt:.1f} s wall on {cores} processes"}
         result["cpu_c_port"] = {"value": c_v, "unit": "fits/s", "cores": cores,
