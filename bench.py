@@ -391,8 +391,8 @@ def run_ours(args):
         e2e_s += max_over_ranks(time.perf_counter() - a)
         chunks = r.stats["n_chunks"]
     e2e_value = count * world * e2e_steps / e2e_s
-    # the same public call with 16-bit camera counts (sf_fit_batch_u16: half the PCIe bytes, widened on the
-    # device); reported beside the headline, which streams the reference's float32 layout
+    # the same public call with 16-bit camera counts (sf_fit_batch_u16: half the PCIe bytes, staged as u16
+    # and widened by the fit kernel); reported beside the headline, which streams the reference's float32 layout
     e2e_u16 = None
     if np.array_equal(images, np.round(images)) and images.max(initial=0) < 65536 and images.min(initial=0) >= 0:
         pin_u16 = torch.from_numpy(images.astype(np.uint16)).pin_memory()
@@ -406,7 +406,7 @@ def run_ours(args):
             u16_s += max_over_ranks(time.perf_counter() - a)
         e2e_u16 = {"value": count * world * e2e_steps / u16_s, "unit": "fits/s",
                    "h2d_bytes_per_step": count * (N * 2 + model * 4), "d2h_bytes_per_step": count * (model * 4 + 14),
-                   "path": "fit_batch(uint16 images) -> sf_fit_batch_u16 (u16 over PCIe, widened to f32 on device)"}
+                   "path": "fit_batch(uint16 images) -> sf_fit_batch_u16 (u16 over PCIe, staged as u16 and widened in the fit kernel)"}
 
     # ---- parity on a sample (GPU vs C oracle, bitwise) and CPU baselines (rank 0)
     result = {}

@@ -96,7 +96,7 @@ int sf_fit_batch(const float* images, int32_t width, int32_t height, int64_t cou
 /*
  * sf_fit_batch_u16 -- sf_fit_batch for 16-bit camera counts: images [count][H][W]
  * uint16 (host pointers).  Each chunk is copied as u16 (half the PCIe bytes of
- * f32) and widened to f32 on the device (exact), so results are identical to
+ * f32) and staged as u16 by the fit kernel, which widens each pixel exactly, so results are identical to
  * sf_fit_batch on the same values as float32.
  */
 int sf_fit_batch_u16(const uint16_t* images, int32_t width, int32_t height, int64_t count, const float* inits,

@@ -138,7 +138,7 @@ struct Slot {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[4] = {};  // start, h2d done, kernel done, d2h done
   float* d_img = nullptr;
-  uint16_t* d_img16 = nullptr;  // 16-bit chunk before widening (sf_fit_batch_u16)
+  uint16_t* d_img16 = nullptr;  // 16-bit chunk (sf_fit_batch_u16), read as u16 by the fit kernel
   float* d_init = nullptr;
   float* d_par = nullptr;
   float* d_a = nullptr;
@@ -314,6 +314,17 @@ int run_shard(int dev, HostJob& j) {
   if (ensure_ctx(*c, dev, (size_t)chunk, N, P, staging) != 0) return -1;
   SF_CUDA(cudaMemsetAsync(c->d_evals, 0, 3 * sizeof(unsigned long long), c->slot[0].stream));
   SF_CUDA(cudaStreamSynchronize(c->slot[0].stream));
+  // SPOTFIT_TRACE=1: per-chunk device timeline on stderr (diagnostic; tools/e2e_sweep.py)
+  static const bool trace = std::getenv("SPOTFIT_TRACE") != nullptr;
+  std::vector<cudaEvent_t> tev;
+  auto mark = [&](cudaStream_t st) -> cudaError_t {
+    if (!trace) return cudaSuccess;
+    cudaEvent_t e;
+    const cudaError_t r = cudaEventCreate(&e);
+    if (r != cudaSuccess) return r;
+    tev.push_back(e);
+    return cudaEventRecord(e, st);
+  };
   for (size_t ci = 0; ci < chunks.size(); ++ci) {
     Slot& s = c->slot[ci % kStreams];
     const int64_t lo = j.lo + chunks[ci].first;
@@ -323,6 +334,7 @@ int run_shard(int dev, HostJob& j) {
       copy_out_staged(s, j);
     }
     SF_CUDA(cudaEventRecord(s.ev[0], s.stream));
+    SF_CUDA(mark(s.stream));
     const size_t px_bytes = j.images16 ? sizeof(uint16_t) : sizeof(float);
     const void* src_img = j.images16 ? (const void*)(j.images16 + lo * N) : (const void*)(j.images + lo * N);
     const float* src_init = j.inits + lo * P;
@@ -332,16 +344,22 @@ int run_shard(int dev, HostJob& j) {
       src_img = s.h_in;
       src_init = s.h_in + s.cap_spots * N;
     }
+    // inits first, then pixels: the fit needs nothing else, so it can start (and fill the previous
+    // fit's tail) as soon as the copy engine is done.  (A widening kernel between the two copies
+    // made the init copy wait behind the next chunks' pixel copies: tools/e2e_trace.py.)
+    SF_CUDA(cudaMemcpyAsync(s.d_init, src_init, n * P * sizeof(float), cudaMemcpyHostToDevice, s.stream));
     if (j.images16) {
       SF_CUDA(cudaMemcpyAsync(s.d_img16, src_img, n * N * px_bytes, cudaMemcpyHostToDevice, s.stream));
-      SF_CUDA(sf::launch_widen_u16(s.d_img16, s.d_img, n * N, s.stream));
+      SF_CUDA(mark(s.stream));
     } else {
       SF_CUDA(cudaMemcpyAsync(s.d_img, src_img, n * N * px_bytes, cudaMemcpyHostToDevice, s.stream));
+      SF_CUDA(mark(s.stream));
     }
-    SF_CUDA(cudaMemcpyAsync(s.d_init, src_init, n * P * sizeof(float), cudaMemcpyHostToDevice, s.stream));
     SF_CUDA(cudaEventRecord(s.ev[1], s.stream));
+    SF_CUDA(mark(s.stream));
     sf::LaunchFit a;
     a.images = s.d_img;
+    a.images16 = j.images16 ? s.d_img16 : nullptr;  // staged as u16 by the fit kernel itself
     a.inits = s.d_init;
     a.count = n;
     a.geom = geom;
@@ -351,6 +369,7 @@ int run_shard(int dev, HostJob& j) {
     a.sm_count = c->sms;
     if (dispatch_fit(P, a) != 0) return -1;
     SF_CUDA(cudaEventRecord(s.ev[2], s.stream));
+    SF_CUDA(mark(s.stream));
     if (j.pinned_out) {
       SF_CUDA(cudaMemcpyAsync(j.par + lo * P, s.d_par, n * P * sizeof(float), cudaMemcpyDeviceToHost, s.stream));
       SF_CUDA(cudaMemcpyAsync(j.alpha + lo, s.d_a, n * sizeof(float), cudaMemcpyDeviceToHost, s.stream));
@@ -373,11 +392,20 @@ int run_shard(int dev, HostJob& j) {
       s.p_n = n;
     }
     SF_CUDA(cudaEventRecord(s.ev[3], s.stream));
+    SF_CUDA(mark(s.stream));
     ++j.chunks;
   }
   for (auto& s : c->slot) {
     SF_CUDA(cudaStreamSynchronize(s.stream));
     if (staging) copy_out_staged(s, j);
+  }
+  if (trace && !tev.empty()) {  // per chunk: start, H2D images, H2D inits (+widen), fit, D2H (ms from chunk 0)
+    for (size_t i = 0; i < tev.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, tev[0], tev[i]);
+      std::fprintf(stderr, "%s%.3f%s", i % 5 == 0 ? "TRACE " : "", ms, i % 5 == 4 ? "\n" : " ");
+    }
+    for (auto e : tev) cudaEventDestroy(e);
   }
   SF_CUDA(cudaMemcpy(j.evals, c->d_evals, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
   return 0;

@@ -279,12 +279,14 @@ struct LaneSetup {
   }
 };
 
-template <int P, int SLOTS, bool FULL>
+// PX: pixel type of `images` -- float, or uint16_t camera counts (sf_fit_batch_u16), staged as
+// u16 and widened exactly in load_spot, so the host pipeline needs no separate widening kernel
+template <int P, int SLOTS, bool FULL, typename PX = float>
 __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
                                   P == 5 ? (SLOTS >= 8 ? 1 : SF_MINB_P5)
                                          : (SLOTS == 8 ? 2 * SF_MINB_P3 : (SLOTS == 16 ? SF_MINB_P3
                                                                                      : (P == 3 ? SF_MINB_P3 : SF_MINB_P4))))
-    fit_kernel(const float* __restrict__ images, const float* __restrict__ inits, int64_t count, const Geom geom,
+    fit_kernel(const PX* __restrict__ images, const float* __restrict__ inits, int64_t count, const Geom geom,
                const Cfg cfg, FitOut out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem<P, SLOTS> S;
@@ -318,7 +320,7 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
   const uintptr_t lo = (uintptr_t)images, hi = (uintptr_t)(images + count * (int64_t)N);
   auto prefetch = [&](int64_t sp) {
     if (sp < count) {
-      nsh = stage_spot<P, SLOTS>(S, gib, L.gl, images + sp * (int64_t)N, lo, hi, N);
+      nsh = stage_spot<P, SLOTS, PX>(S, gib, L.gl, images + sp * (int64_t)N, lo, hi, N);
 #pragma unroll
       for (int k = 0; k < P; ++k) nxt[k] = __ldg(inits + sp * P + k);
     }
@@ -381,7 +383,8 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
       // f32 values cannot overflow f64), so it doubles as the InvalidInput pixel check
       bool sgt, sg40;
       const double gsum =
-          load_spot<P, SLOTS, FULL>(S, S.stage + gib * S.sw + nsh, load, L.own, L.base, L.tbase, L.ch, L.tl, sgt, sg40);
+          load_spot<P, SLOTS, FULL, PX>(S, reinterpret_cast<const PX*>(S.stage + gib * S.sw) + nsh, load, L.own,
+                                        L.base, L.tbase, L.ch, L.tl, sgt, sg40);
       group_sync<SLOTS>();  // the staging window has been read: refill it
       const int64_t nxt_spot = claim(load);
       if (load) {

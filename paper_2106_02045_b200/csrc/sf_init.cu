@@ -109,31 +109,6 @@ cudaError_t launch_estimate_initial(const float* images, int W, int H, int64_t c
   return cudaGetLastError();
 }
 
-// 16-bit camera counts -> f32 (exact), 8 pixels per thread
-__global__ void widen_u16_kernel(const uint16_t* __restrict__ in, float* __restrict__ out, int64_t n) {
-  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
-  if (i + 8 <= n && (((uintptr_t)(in + i)) & 15) == 0) {
-    const uint4 v = *reinterpret_cast<const uint4*>(in + i);
-    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-    float4 a, b;
-    a.x = (float)(w[0] & 0xffffu); a.y = (float)(w[0] >> 16); a.z = (float)(w[1] & 0xffffu); a.w = (float)(w[1] >> 16);
-    b.x = (float)(w[2] & 0xffffu); b.y = (float)(w[2] >> 16); b.z = (float)(w[3] & 0xffffu); b.w = (float)(w[3] >> 16);
-    if ((((uintptr_t)(out + i)) & 15) == 0) {
-      *reinterpret_cast<float4*>(out + i) = a;
-      *reinterpret_cast<float4*>(out + i + 4) = b;
-      return;
-    }
-  }
-  for (int64_t k = i; k < i + 8 && k < n; ++k) out[k] = (float)in[k];
-}
-
-cudaError_t launch_widen_u16(const uint16_t* in, float* out, int64_t n, cudaStream_t stream) {
-  if (n <= 0) return cudaSuccess;
-  const int64_t threads = (n + 7) / 8;
-  widen_u16_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, stream>>>(in, out, n);
-  return cudaGetLastError();
-}
-
 // Exhaustive-check helper: numpy exp on the device (variant 0: production
 // scalar npexp, 1: the same with CUDA's IEEE __fdiv_rn, 2: the packed f32x2
 // npexp2 of the chain loops, on element pairs (x[2i], x[2i+1])).

@@ -13,8 +13,9 @@
 
 namespace sf {
 
-int SF_UNIT_NAME(launch_fit, SF_P, SF_SLOTS)(const LaunchFit& a, cudaError_t* err) {
-  auto kern = a.geom.full ? fit_kernel<SF_P, SF_SLOTS, true> : fit_kernel<SF_P, SF_SLOTS, false>;
+template <typename PX>
+static int launch_fit_px(const LaunchFit& a, const PX* images, cudaError_t* err) {
+  auto kern = a.geom.full ? fit_kernel<SF_P, SF_SLOTS, true, PX> : fit_kernel<SF_P, SF_SLOTS, false, PX>;
   constexpr int tpb = threads_per_block<SF_SLOTS>();
   constexpr int groups_per_block = SF_SLOTS >= 8 ? 1 : (tpb / 32) * (32 / (8 * SF_SLOTS));
   const size_t smem = Smem<SF_P, SF_SLOTS>::bytes(a.geom.ch, a.geom.tl, a.geom.N);
@@ -28,9 +29,13 @@ int SF_UNIT_NAME(launch_fit, SF_P, SF_SLOTS)(const LaunchFit& a, cudaError_t* er
   const int64_t need = (a.count + groups_per_block - 1) / groups_per_block;
   if (blocks > need) blocks = need;
   if (blocks < 1) return 0;
-  kern<<<(unsigned)blocks, tpb, smem, a.stream>>>(a.images, a.inits, a.count, a.geom, a.cfg, a.out);
+  kern<<<(unsigned)blocks, tpb, smem, a.stream>>>(images, a.inits, a.count, a.geom, a.cfg, a.out);
   *err = cudaGetLastError();
   return (int)blocks;
+}
+
+int SF_UNIT_NAME(launch_fit, SF_P, SF_SLOTS)(const LaunchFit& a, cudaError_t* err) {
+  return a.images16 ? launch_fit_px<uint16_t>(a, a.images16, err) : launch_fit_px<float>(a, a.images, err);
 }
 
 #if SF_P != 5  // model-level evaluation exists for the implicit models only

@@ -10,6 +10,7 @@ namespace sf {
 
 struct LaunchFit {
   const float* images;
+  const uint16_t* images16 = nullptr;  // non-null: 16-bit pixels (fit_kernel<..., uint16_t>), images unused
   const float* inits;
   int64_t count;
   Geom geom;
@@ -58,8 +59,6 @@ cudaError_t launch_estimate_initial(const float* images, int W, int H, int64_t c
 cudaError_t launch_simulate(const sf_sim_config& c, int W, int H, int64_t first, int64_t count, float* images,
                             float* truth, cudaStream_t stream);
 
-// u16 -> f32 widening of a streamed chunk (sf_init.cu; sf_fit_batch_u16)
-cudaError_t launch_widen_u16(const uint16_t* in, float* out, int64_t n, cudaStream_t stream);
 
 // shared-divisor f64 division check (sf_init.cu)
 cudaError_t launch_ddiv(const double* a, const double* b, double* out, int64_t n, cudaStream_t stream);
