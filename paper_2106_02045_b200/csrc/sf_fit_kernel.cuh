@@ -35,8 +35,9 @@ static __device__ unsigned long long g_work[kWorkSlots][2];
 
 // Per-spot LM state, replicated in every lane of the group.  The normal system
 // at `best` (needed again only for lambda retries) lives in the group's shared
-// slot `sys`: every lane writes the identical values and reads back only its
-// own writes, so no synchronisation is needed.
+// slot `sys`: every lane holds the identical system, one lane per (group, warp)
+// stores it (sys_writer) and __syncwarp(gmask) publishes it to the group's other
+// lanes (compute-sanitizer racecheck clean: profiles/r01_compute_sanitizer.txt).
 template <int P>
 struct LMState {
   float p[P];     // parameters under evaluation (G point or trial point)
