@@ -210,10 +210,13 @@ def run_reference(args):
     return 0
 
 
-def realtime(args, dev):
+def realtime(args, dev, zero_copy=True):
     """C5 real-time mode (BASELINE.json configs[4]): 50 spots/frame, 1000 frames,
-    per-frame latency of host frame -> H2D -> GPU initializer -> LM fit -> D2H,
-    replayed as one CUDA graph per frame (host clock around each blocking frame)."""
+    per-frame latency of host frame -> GPU initializer -> LM fit -> results on the host,
+    replayed as one CUDA graph per frame (host clock around each blocking frame).
+    zero_copy: the kernels read the frame from, and write the results to, pinned
+    (device-mapped) host memory, so the graph is two kernel nodes; otherwise an
+    explicit H2D copy, the kernels on device buffers and D2H copies."""
     import ctypes
 
     import torch
@@ -230,26 +233,40 @@ def realtime(args, dev):
     L = _lib.lib()
     allimg = make_workload(W, H, spf * frames, 3, seed=4242).reshape(frames, spf, W * H)
     pin_in = torch.empty((spf, W * H), dtype=torch.float32).pin_memory()
-    pin_out = torch.empty((spf, 3 + 3), dtype=torch.float32).pin_memory()
     pin_u8 = torch.empty((2, spf), dtype=torch.uint8).pin_memory()
     d_img = torch.empty((spf, W * H), dtype=torch.float32, device=dev)
     d_ini = torch.empty((spf, 3), dtype=torch.float32, device=dev)
-    d_out = torch.empty((spf, 6), dtype=torch.float32, device=dev)
+    d_par = torch.empty((spf, 3), dtype=torch.float32, device=dev)
     d_u8 = torch.empty((2, spf), dtype=torch.uint8, device=dev)
     d_ab = torch.empty((3, spf), dtype=torch.float32, device=dev)
     stream = torch.cuda.Stream(dev)
+    h_ab = torch.empty((3, spf), dtype=torch.float32).pin_memory()
+    h_par = torch.empty((spf, 3), dtype=torch.float32).pin_memory()
 
-    def frame_ops():
+    def frame_ops_zero_copy():
+        st = torch.cuda.current_stream(dev).cuda_stream
+        _lib.check(L.sf_estimate_initial_device(pin_in.data_ptr(), W, H, spf, 3, b.sigma_min, b.sigma_max,
+                                                d_ini.data_ptr(), None, st))
+        _lib.check(L.sf_fit_batch_device(pin_in.data_ptr(), W, H, spf, d_ini.data_ptr(), ctypes.byref(ccfg),
+                                         h_par.data_ptr(), h_ab[0].data_ptr(), h_ab[1].data_ptr(),
+                                         h_ab[2].data_ptr(), pin_u8[0].data_ptr(), pin_u8[1].data_ptr(), None, st))
+
+    def frame_ops_copy():
         st = torch.cuda.current_stream(dev).cuda_stream
         d_img.copy_(pin_in, non_blocking=True)
         _lib.check(L.sf_estimate_initial_device(d_img.data_ptr(), W, H, spf, 3, b.sigma_min, b.sigma_max,
                                                 d_ini.data_ptr(), None, st))
         _lib.check(L.sf_fit_batch_device(d_img.data_ptr(), W, H, spf, d_ini.data_ptr(), ctypes.byref(ccfg),
-                                         d_out.data_ptr(), d_ab[0].data_ptr(), d_ab[1].data_ptr(),
+                                         d_par.data_ptr(), d_ab[0].data_ptr(), d_ab[1].data_ptr(),
                                          d_ab[2].data_ptr(), d_u8[0].data_ptr(), d_u8[1].data_ptr(), None, st))
-        d_out[:, 3:].copy_(d_ab.t())
-        pin_out.copy_(d_out, non_blocking=True)
+        h_par.copy_(d_par, non_blocking=True)
+        h_ab.copy_(d_ab, non_blocking=True)
         pin_u8.copy_(d_u8, non_blocking=True)
+
+    frame_ops = frame_ops_zero_copy if zero_copy else frame_ops_copy
+
+    def frame_result():
+        return h_par.numpy().copy(), h_ab.numpy().T.copy(), pin_u8.numpy().copy()
 
     with torch.cuda.stream(stream):
         for _ in range(3):
@@ -267,19 +284,28 @@ def realtime(args, dev):
     for f in range(frames):
         t0 = time.perf_counter()
         pin_in.numpy()[:] = allimg[f]  # the camera frame lands in pinned staging
-        if graph is not None:
-            graph.replay()
-        else:
-            with torch.cuda.stream(stream):
+        with torch.cuda.stream(stream):  # CUDAGraph.replay launches on the current stream
+            if graph is not None:
+                graph.replay()
+            else:
                 frame_ops()
         stream.synchronize()
         lat.append(time.perf_counter() - t0)
     lat_us = np.array(lat) * 1e6
+    # the last frame's results equal the batch API's on the same spots (bitwise)
+    par, ab, u8 = frame_result()
+    ref = sf.fit_batch(allimg[frames - 1], grid=grid)
+    same = (np.array_equal(par.view(np.uint32), np.asarray(ref.params).view(np.uint32))
+            and np.array_equal(ab[:, 0].view(np.uint32), np.asarray(ref.alpha).view(np.uint32))
+            and np.array_equal(u8[0], np.asarray(ref.status)) and np.array_equal(u8[1], np.asarray(ref.iterations)))
     return {"spots_per_frame": spf, "frames": frames, "grid": f"{W}x{H}", "cuda_graph": graph is not None,
+            "zero_copy": zero_copy, "matches_fit_batch": bool(same),
             "p50_us": float(np.percentile(lat_us, 50)), "p99_us": float(np.percentile(lat_us, 99)),
             "max_us": float(lat_us.max()), "mean_us": float(lat_us.mean()),
             "sustains_1kHz": bool(np.percentile(lat_us, 99) < 1000.0),
-            "span": "host frame copy -> H2D -> GPU initializer -> LM fit -> D2H (blocking per frame)"}
+            "span": ("host frame copy -> GPU initializer + LM fit reading the pinned frame over PCIe and writing "
+                     "the results to pinned host memory (blocking per frame)") if zero_copy else
+                    "host frame copy -> H2D -> GPU initializer -> LM fit -> D2H (blocking per frame)"}
 
 
 def run_ours(args):
@@ -411,7 +437,7 @@ def run_ours(args):
     # ---- parity on a sample (GPU vs C oracle, bitwise) and CPU baselines (rank 0)
     result = {}
     if rank == 0 and args.rt_frames > 0:
-        result["realtime"] = realtime(args, dev)
+        result["realtime"] = realtime(args, dev, zero_copy=not args.rt_copy)
     if rank == 0:
         from oracle import lm, oracle_c
 
@@ -537,6 +563,7 @@ def main(argv=None):
     ap.add_argument("--profile", action="store_true", help="kernel leg only (for ncu); prints no bench line")
     ap.add_argument("--rt-spots", type=int, default=50, help="real-time mode: spots per frame (C5)")
     ap.add_argument("--rt-frames", type=int, default=1000, help="real-time mode frames (0 disables)")
+    ap.add_argument("--rt-copy", action="store_true", help="real-time mode with explicit H2D/D2H copies")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3
