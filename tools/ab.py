@@ -16,9 +16,11 @@ sys.path.insert(0, %r)
 import paper_2106_02045_b200 as sf
 from oracle import lm, oracle_c
 W = H = int(sys.argv[1]); model = int(sys.argv[2])
-im, _ = sf.simulate_batch(sf.SimConfig(width=W, height=H, count=20000, seed=77, model=model))
-ini, _ = sf.estimate_initial_batch(im, model)
-r = sf.fit_batch(im, ini, engine="implicit3" if model == 3 else "elliptical")
+im, _ = sf.simulate_batch(sf.SimConfig(width=W, height=H, count=20000, seed=77, model=min(model, 4)))
+ini, amps = sf.estimate_initial_batch(im, 4 if model == 4 else 3)
+if model == 5:  # explicit-5: (x, y, sigma) + the initializer's (alpha, beta)
+    ini = np.ascontiguousarray(np.concatenate([ini, amps], axis=1).astype(np.float32))
+r = sf.fit_batch(im, ini, engine={3: "implicit3", 4: "elliptical", 5: "explicit5"}[model])
 ref = oracle_c.fit_batch(im.reshape(20000, -1), ini, W, H, lm.LMConfig.for_grid(W, H))
 ok = all(np.array_equal(np.asarray(getattr(r, k)).view(np.uint8), np.asarray(ref[k]).view(np.uint8))
          for k in ("params", "alpha", "beta", "nchi2", "status", "iterations"))
@@ -37,7 +39,7 @@ def run(lib, config="c2", count=1000000):
     except Exception:
         v = None
         sys.stderr.write(out.stdout[-2000:] + out.stderr[-2000:])
-    W, model = {"c2": (15, 3), "c1": (11, 3), "c3": (21, 4), "c4": (32, 3)}[config]
+    W, model = {"c2": (15, 3), "c1": (11, 3), "c3": (21, 4), "c4": (32, 3), "c2x": (15, 5)}[config]
     p = subprocess.run([sys.executable, "-c", PARITY, str(W), str(model)], capture_output=True, text=True, env=env)
     ok = "PARITY True" in p.stdout
     if not ok:
