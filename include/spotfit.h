@@ -109,7 +109,10 @@ int sf_fit_batch_u16(const uint16_t* images, int32_t width, int32_t height, int6
  * the current device, launched on `stream` (cudaStream_t, 0 = legacy default),
  * asynchronous.  Used by bench.py for the HBM-resident measurement and by
  * callers that already hold spots on the GPU.  evals_out: device u64[3]
- * accumulating (G-evals, T-evals, kernel evals) or NULL.
+ * accumulating (G-evals, T-evals, kernel evals) or NULL.  Any device-accessible
+ * address works, including pinned host memory (device-mapped under UVA): small
+ * latency-bound frames read the spots and write the results over PCIe directly
+ * (bench.py realtime, zero copy).  sf_estimate_initial_device likewise.
  */
 int sf_fit_batch_device(const float* d_images, int32_t width, int32_t height, int64_t count, const float* d_inits,
                         const sf_config* cfg, float* d_params, float* d_alpha, float* d_beta, float* d_nchi2,
