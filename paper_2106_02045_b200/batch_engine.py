@@ -82,6 +82,8 @@ def _as_image_array(images, grid: Optional[PixelGrid]):
     try:
         import torch
 
+        if isinstance(images, torch.Tensor) and not images.is_cuda:
+            images = images.numpy()  # host tensors take the streamed host path, like numpy arrays
         if isinstance(images, torch.Tensor):
             if grid is None:
                 if images.dim() != 3:
