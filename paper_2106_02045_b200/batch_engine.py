@@ -164,6 +164,8 @@ def fit_batch(images, inits=None, config: FitConfig = FitConfig(), engine: str =
 
         ini = _auto_inits(torch.as_tensor(imgs.astype(np.float32, copy=False)).cuda(), grid, P, config).cpu().numpy()
     else:
+        if hasattr(inits, "is_cuda") and inits.is_cuda:  # device inits with host images
+            inits = inits.cpu()
         ini = np.ascontiguousarray(params_array(inits), dtype=np.float32).reshape(count, P)
     if out is None:
         out = BatchResult(np.empty((count, P), np.float32), np.empty(count, np.float32), np.empty(count, np.float32),
