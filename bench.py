@@ -179,7 +179,7 @@ def run_reference(args):
     from oracle import initializer as oinit
 
     cores = len(os.sched_getaffinity(0))
-    sample = args.ref_sample or max(2000, 500 * cores)
+    sample = args.ref_sample or max(4000, 1500 * cores)
     images = make_workload(W, H, sample, model, seed=2021)
     inits, amps = oinit.estimate_initial_batch(images, W, H, 0.3, float(max(W, H)), min(model, 4))
     if model == 5:
@@ -458,14 +458,14 @@ def run_ours(args):
                             "state_identical_frac": float((u8[0][sample_idx] == ref["status"]).mean()),
                             "checker": "oracle/spotfit_oracle.c (pinned to reference model.py fixtures)"}
         cores = len(os.sched_getaffinity(0))
-        samp = args.ref_sample or max(2000, 500 * cores)
+        samp = args.ref_sample or max(4000, 1500 * cores)
         cpu_v, cpu_dt, kind = cpu_reference(W, H, model, images, ini, samp, cores)
         c_v = cpu_c_port(W, H, images, ini, min(count, 20 * samp), cores)
         src = ("the unmodified reference spotfit.model (baseline/_ref)" if kind == "reference"
                else "oracle/model_np.py (restated reference numpy arithmetic)")
         result["cpu_baseline"] = {"value": cpu_v, "unit": "fits/s", "cores": cores, "kind": kind, "host": host_info(),
                                   "sample": f"{samp} spots of this workload, LM loop oracle/lm.py over {src}, "
-                                            f"{cpu_dt:.1f} s wall on {cores} processes"}
+                                            f"{cpu_dt:.1f} s wall on {cores} processes (~{cpu_dt * cores:.0f} s of CPU work)"}
         result["cpu_c_port"] = {"value": c_v, "unit": "fits/s", "cores": cores,
                                 "note": "bit-exact C restatement (oracle/spotfit_oracle.c), stronger CPU comparator"}
 
