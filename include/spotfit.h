@@ -119,6 +119,18 @@ int sf_fit_batch_device(const float* d_images, int32_t width, int32_t height, in
                         uint8_t* d_status, uint8_t* d_iters, uint64_t* d_evals, void* stream);
 
 /*
+ * sf_fit_batch_device_u16 -- sf_fit_batch_device for 16-bit camera counts
+ * [count][H][W] uint16 in device-accessible memory: the fit kernel stages the
+ * u16 pixels itself and widens them exactly (no f32 copy), so results equal
+ * sf_fit_batch_device on the same values as float32.  Extension (not in the
+ * reference interface), the device-side twin of sf_fit_batch_u16.
+ */
+int sf_fit_batch_device_u16(const uint16_t* d_images, int32_t width, int32_t height, int64_t count,
+                            const float* d_inits, const sf_config* cfg, float* d_params, float* d_alpha,
+                            float* d_beta, float* d_nchi2, uint8_t* d_status, uint8_t* d_iters, uint64_t* d_evals,
+                            void* stream);
+
+/*
  * sf_eval_batch_device -- model-level evaluation at given shape parameters
  * (one evaluation per spot, no LM): replaces the spotfit.model call chain
  * profile_and_gradient -> alpha_beta -> chi_squared -> gradient_sums ->

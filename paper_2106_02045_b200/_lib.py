@@ -100,6 +100,8 @@ SYMBOLS = {
                                         _vp, _vp, _vp, _i32, ctypes.POINTER(sf_stats)]),
     "sf_fit_batch_device": (ctypes.c_int, [_vp, _i32, _i32, _i64, _vp, ctypes.POINTER(sf_config), _vp, _vp, _vp, _vp,
                                            _vp, _vp, _vp, _vp]),
+    "sf_fit_batch_device_u16": (ctypes.c_int, [_vp, _i32, _i32, _i64, _vp, ctypes.POINTER(sf_config), _vp, _vp, _vp,
+                                               _vp, _vp, _vp, _vp, _vp]),
     "sf_eval_batch_device": (ctypes.c_int, [_vp, _i32, _i32, _i64, _i32, _vp, _vp, _vp]),
     "sf_estimate_initial_device": (ctypes.c_int, [_vp, _i32, _i32, _i64, _i32, _f64, _f64, _vp, _vp, _vp]),
     "sf_simulate_host": (ctypes.c_int, [ctypes.POINTER(sf_sim_config), _i32, _i32, _i64, _i64, _vp, _vp, _i32]),

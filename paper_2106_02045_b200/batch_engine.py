@@ -90,7 +90,7 @@ def _as_image_array(images, grid: Optional[PixelGrid]):
                     raise ValueError("pass grid= for flattened image tensors")
                 grid = PixelGrid(images.shape[2], images.shape[1])
             t = images.reshape(images.shape[0], -1)
-            if t.dtype != torch.float32:
+            if t.dtype not in (torch.float32, torch.uint16):  # u16 counts: sf_fit_batch_device_u16
                 t = t.float()
             return t.contiguous(), grid
     except ImportError:
@@ -140,8 +140,9 @@ def fit_batch(images, inits=None, config: FitConfig = FitConfig(), engine: str =
         import torch
 
         dev = imgs.device
+        u16 = imgs.dtype == torch.uint16
         if inits is None:
-            ini = _auto_inits(imgs, grid, P, config)
+            ini = _auto_inits(imgs.float() if u16 else imgs, grid, P, config)
         else:
             ini = torch.as_tensor(params_array(inits) if not isinstance(inits, torch.Tensor) else inits,
                                   dtype=torch.float32, device=dev).reshape(count, P).contiguous()
@@ -150,9 +151,10 @@ def fit_batch(images, inits=None, config: FitConfig = FitConfig(), engine: str =
         u8 = torch.empty((2, count), dtype=torch.uint8, device=dev)
         ev = torch.zeros(3, dtype=torch.int64, device=dev)
         stream = torch.cuda.current_stream(dev).cuda_stream
-        _lib.check(L.sf_fit_batch_device(imgs.data_ptr(), grid.width, grid.height, count, ini.data_ptr(),
-                                         ctypes.byref(ccfg), par.data_ptr(), fl[0].data_ptr(), fl[1].data_ptr(),
-                                         fl[2].data_ptr(), u8[0].data_ptr(), u8[1].data_ptr(), ev.data_ptr(), stream))
+        entry = L.sf_fit_batch_device_u16 if u16 else L.sf_fit_batch_device
+        _lib.check(entry(imgs.data_ptr(), grid.width, grid.height, count, ini.data_ptr(), ctypes.byref(ccfg),
+                         par.data_ptr(), fl[0].data_ptr(), fl[1].data_ptr(), fl[2].data_ptr(), u8[0].data_ptr(),
+                         u8[1].data_ptr(), ev.data_ptr(), stream))
         torch.cuda.current_stream(dev).synchronize()
         evs = ev.cpu().tolist()
         return BatchResult(par.cpu().numpy(), fl[0].cpu().numpy(), fl[1].cpu().numpy(), fl[2].cpu().numpy(),

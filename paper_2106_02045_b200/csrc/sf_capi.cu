@@ -484,20 +484,23 @@ void sf_host_free(void* p) {
   if (p) cudaFreeHost(p);
 }
 
-int sf_fit_batch_device(const float* d_images, int32_t width, int32_t height, int64_t count, const float* d_inits,
-                        const sf_config* cfg, float* d_params, float* d_alpha, float* d_beta, float* d_nchi2,
-                        uint8_t* d_status, uint8_t* d_iters, uint64_t* d_evals, void* stream) {
+static int fit_device_impl(const float* d_images, const uint16_t* d_images16, int32_t width, int32_t height,
+                           int64_t count, const float* d_inits, const sf_config* cfg, float* d_params, float* d_alpha,
+                           float* d_beta, float* d_nchi2, uint8_t* d_status, uint8_t* d_iters, uint64_t* d_evals,
+                           void* stream) {
   if (check_grid(width, height) != 0) return -1;
   if (count < 0) return fail("negative count");
   sf::Cfg kc;
   if (make_cfg(cfg, width, height, kc) != 0) return -1;
   if (count == 0) return 0;
-  if (!d_images || !d_inits || !d_params || !d_alpha || !d_beta || !d_nchi2 || !d_status || !d_iters)
+  if ((!d_images && !d_images16) || !d_inits || !d_params || !d_alpha || !d_beta || !d_nchi2 || !d_status ||
+      !d_iters)
     return fail("NULL buffer");
   sf::Geom geom;
   sf::build_geom(width, height, cfg->model, geom);
   sf::LaunchFit a;
   a.images = d_images;
+  a.images16 = d_images16;
   a.inits = d_inits;
   a.count = count;
   a.geom = geom;
@@ -507,6 +510,22 @@ int sf_fit_batch_device(const float* d_images, int32_t width, int32_t height, in
   a.stream = static_cast<cudaStream_t>(stream);
   a.sm_count = sm_count_of_current();
   return dispatch_fit(cfg->model, a);
+}
+
+int sf_fit_batch_device(const float* d_images, int32_t width, int32_t height, int64_t count, const float* d_inits,
+                        const sf_config* cfg, float* d_params, float* d_alpha, float* d_beta, float* d_nchi2,
+                        uint8_t* d_status, uint8_t* d_iters, uint64_t* d_evals, void* stream) {
+  return fit_device_impl(d_images, nullptr, width, height, count, d_inits, cfg, d_params, d_alpha, d_beta, d_nchi2,
+                         d_status, d_iters, d_evals, stream);
+}
+
+int sf_fit_batch_device_u16(const uint16_t* d_images, int32_t width, int32_t height, int64_t count,
+                            const float* d_inits, const sf_config* cfg, float* d_params, float* d_alpha,
+                            float* d_beta, float* d_nchi2, uint8_t* d_status, uint8_t* d_iters, uint64_t* d_evals,
+                            void* stream) {
+  if (!d_images && count > 0) return fail("NULL buffer");
+  return fit_device_impl(nullptr, d_images, width, height, count, d_inits, cfg, d_params, d_alpha, d_beta, d_nchi2,
+                         d_status, d_iters, d_evals, stream);
 }
 
 int sf_eval_batch_device(const float* d_images, int32_t width, int32_t height, int64_t count, int32_t model,
