@@ -24,10 +24,11 @@ def log_uniform(rng, lo, hi):
     return float(10.0 ** rng.uniform(np.log10(lo), np.log10(hi)))
 
 
-def one_round(rng, r):
+def make_case(rng, models=(3, 3, 4, 5), counts=(200, 3000)):
+    """One random case: grid, model, FitConfig kwargs + bounds (GPU and oracle forms), images, inits."""
     W, H = int(rng.integers(1, 33)), int(rng.integers(1, 33))
-    model = int(rng.choice([3, 3, 4, 5]))
-    count = int(rng.integers(200, 3000))
+    model = int(rng.choice(list(models)))
+    count = int(rng.integers(*counts))
     S = max(W, H)
     smin = float(rng.uniform(0.1, 0.8))
     kw = dict(max_iterations=int(rng.integers(1, 41)),
@@ -55,6 +56,13 @@ def one_round(rng, r):
     if model == 5:
         ini = np.concatenate([ini, amps], axis=1)
     ini = np.ascontiguousarray(ini, dtype=np.float32)
+    return dict(W=W, H=H, model=model, count=count, kw=kw, cfg=cfg, ocfg=ocfg, im=im, ini=ini)
+
+
+def one_round(rng, r):
+    c = make_case(rng)
+    W, H, model, count, kw, cfg, ocfg, im, ini = (c[k] for k in ("W", "H", "model", "count", "kw", "cfg", "ocfg",
+                                                                 "im", "ini"))
     engine = {3: "implicit3", 4: "elliptical", 5: "explicit5"}[model]
     res = sf.fit_batch(im, ini, config=cfg, grid=sf.PixelGrid(W, H), engine=engine)
     ref = oracle_c.fit_batch(im, ini, W, H, ocfg)
