@@ -68,6 +68,10 @@ def one_round(rng, r):
     ref = oracle_c.fit_batch(im, ini, W, H, ocfg)
     bad = [k for k in FIELDS if not np.array_equal(np.asarray(getattr(res, k)).view(np.uint8),
                                                    np.asarray(ref[k]).view(np.uint8))]
+    if np.all(im >= 0) and np.all(im < 65536) and np.array_equal(im, np.round(im)):  # camera counts: u16 path too
+        r16 = sf.fit_batch(im.astype(np.uint16), ini, config=cfg, grid=sf.PixelGrid(W, H), engine=engine)
+        bad += [k + "(u16)" for k in FIELDS if not np.array_equal(np.asarray(getattr(r16, k)).view(np.uint8),
+                                                                 np.asarray(ref[k]).view(np.uint8))]
     stops = np.bincount(np.asarray(res.status) & 7, minlength=5)
     print(f"round {r:4d}: {W:2d}x{H:2d} P={model} n={count:4d} it<={kw['max_iterations']:2d} "
           f"stops={stops.tolist()} {'ok' if not bad else 'MISMATCH ' + ','.join(bad)}", flush=True)
