@@ -113,6 +113,10 @@ int sf_fit_batch_u16(const uint16_t* images, int32_t width, int32_t height, int6
  * address works, including pinned host memory (device-mapped under UVA): small
  * latency-bound frames read the spots and write the results over PCIe directly
  * (bench.py realtime, zero copy).  sf_estimate_initial_device likewise.
+ * Each launch holds one of 256 work-claim counters until it ends (round robin),
+ * so at most 256 fit launches may be in flight at once.  A launch captured in a
+ * CUDA graph keeps its counter: replays of one graph must not overlap (replays
+ * on one stream never do).
  */
 int sf_fit_batch_device(const float* d_images, int32_t width, int32_t height, int64_t count, const float* d_inits,
                         const sf_config* cfg, float* d_params, float* d_alpha, float* d_beta, float* d_nchi2,
