@@ -214,9 +214,10 @@ def realtime(args, dev, zero_copy=True):
     """C5 real-time mode (BASELINE.json configs[4]): 50 spots/frame, 1000 frames,
     per-frame latency of host frame -> GPU initializer -> LM fit -> results on the host,
     replayed as one CUDA graph per frame (host clock around each blocking frame).
-    zero_copy: the kernels read the frame from, and write the results to, pinned
-    (device-mapped) host memory, so the graph is two kernel nodes; otherwise an
-    explicit H2D copy, the kernels on device buffers and D2H copies."""
+    The fit kernel estimates the inits itself (fused initializer).  zero_copy: it
+    reads the frame from, and writes the results to, pinned (device-mapped) host
+    memory, so the graph is one kernel node; otherwise an explicit H2D copy, the
+    kernel on device buffers and D2H copies."""
     import ctypes
 
     import torch
@@ -243,20 +244,17 @@ def realtime(args, dev, zero_copy=True):
     h_ab = torch.empty((3, spf), dtype=torch.float32).pin_memory()
     h_par = torch.empty((spf, 3), dtype=torch.float32).pin_memory()
 
+    # inits NULL: the fit kernel estimates each spot's init from the pixels it stages (fused initializer)
     def frame_ops_zero_copy():
         st = torch.cuda.current_stream(dev).cuda_stream
-        _lib.check(L.sf_estimate_initial_device(pin_in.data_ptr(), W, H, spf, 3, b.sigma_min, b.sigma_max,
-                                                d_ini.data_ptr(), None, st))
-        _lib.check(L.sf_fit_batch_device(pin_in.data_ptr(), W, H, spf, d_ini.data_ptr(), ctypes.byref(ccfg),
+        _lib.check(L.sf_fit_batch_device(pin_in.data_ptr(), W, H, spf, None, ctypes.byref(ccfg),
                                          h_par.data_ptr(), h_ab[0].data_ptr(), h_ab[1].data_ptr(),
                                          h_ab[2].data_ptr(), pin_u8[0].data_ptr(), pin_u8[1].data_ptr(), None, st))
 
     def frame_ops_copy():
         st = torch.cuda.current_stream(dev).cuda_stream
         d_img.copy_(pin_in, non_blocking=True)
-        _lib.check(L.sf_estimate_initial_device(d_img.data_ptr(), W, H, spf, 3, b.sigma_min, b.sigma_max,
-                                                d_ini.data_ptr(), None, st))
-        _lib.check(L.sf_fit_batch_device(d_img.data_ptr(), W, H, spf, d_ini.data_ptr(), ctypes.byref(ccfg),
+        _lib.check(L.sf_fit_batch_device(d_img.data_ptr(), W, H, spf, None, ctypes.byref(ccfg),
                                          d_par.data_ptr(), d_ab[0].data_ptr(), d_ab[1].data_ptr(),
                                          d_ab[2].data_ptr(), d_u8[0].data_ptr(), d_u8[1].data_ptr(), None, st))
         h_par.copy_(d_par, non_blocking=True)
@@ -303,9 +301,9 @@ def realtime(args, dev, zero_copy=True):
             "p50_us": float(np.percentile(lat_us, 50)), "p99_us": float(np.percentile(lat_us, 99)),
             "max_us": float(lat_us.max()), "mean_us": float(lat_us.mean()),
             "sustains_1kHz": bool(np.percentile(lat_us, 99) < 1000.0),
-            "span": ("host frame copy -> GPU initializer + LM fit reading the pinned frame over PCIe and writing "
-                     "the results to pinned host memory (blocking per frame)") if zero_copy else
-                    "host frame copy -> H2D -> GPU initializer -> LM fit -> D2H (blocking per frame)"}
+            "span": ("host frame copy -> one fit kernel (fused initializer + LM) reading the pinned frame over PCIe "
+                     "and writing the results to pinned host memory (blocking per frame)") if zero_copy else
+                    "host frame copy -> H2D -> fit kernel (fused initializer + LM) -> D2H (blocking per frame)"}
 
 
 def run_ours(args):

@@ -3,9 +3,11 @@
 Host (numpy) inputs go through ``sf_fit_batch``: contiguous shards per GPU,
 chunked H2D -> kernel -> D2H on overlapped streams, results written in index
 order.  CUDA tensors go through ``sf_fit_batch_device`` on the current torch
-stream.  Missing inits are estimated on the GPU (``sf_estimate_initial_device``,
-SPEC.md:286-290) -- the paper and SPEC time the fit without the initializer
-(PAPER.md:210), so callers that benchmark pass inits explicitly.
+stream.  Missing inits (``inits=None``) are estimated inside the
+fit kernel from the spot it has just staged (sf_fit_kernel.cuh:fused_init): the
+pixels cross PCIe and HBM once, whatever the batch size.  The paper and SPEC time
+the fit without the initializer, so the benchmark's
+headline passes inits explicitly; the fused path is measured beside it.
 """
 from __future__ import annotations
 
@@ -142,7 +144,7 @@ def fit_batch(images, inits=None, config: FitConfig = FitConfig(), engine: str =
         dev = imgs.device
         u16 = imgs.dtype == torch.uint16
         if inits is None:
-            ini = _auto_inits(imgs.float() if u16 else imgs, grid, P, config)
+            ini = None  # fused initializer in the fit kernel
         else:
             ini = torch.as_tensor(params_array(inits) if not isinstance(inits, torch.Tensor) else inits,
                                   dtype=torch.float32, device=dev).reshape(count, P).contiguous()
@@ -150,21 +152,21 @@ def fit_batch(images, inits=None, config: FitConfig = FitConfig(), engine: str =
         fl = torch.empty((3, count), dtype=torch.float32, device=dev)
         u8 = torch.empty((2, count), dtype=torch.uint8, device=dev)
         ev = torch.zeros(3, dtype=torch.int64, device=dev)
-        stream = torch.cuda.current_stream(dev).cuda_stream
-        entry = L.sf_fit_batch_device_u16 if u16 else L.sf_fit_batch_device
-        _lib.check(entry(imgs.data_ptr(), grid.width, grid.height, count, ini.data_ptr(), ctypes.byref(ccfg),
-                         par.data_ptr(), fl[0].data_ptr(), fl[1].data_ptr(), fl[2].data_ptr(), u8[0].data_ptr(),
-                         u8[1].data_ptr(), ev.data_ptr(), stream))
-        torch.cuda.current_stream(dev).synchronize()
+        with torch.cuda.device(dev):  # the library launches on the device that owns the pixels
+            stream = torch.cuda.current_stream(dev).cuda_stream
+            entry = L.sf_fit_batch_device_u16 if u16 else L.sf_fit_batch_device
+            _lib.check(entry(imgs.data_ptr(), grid.width, grid.height, count,
+                             None if ini is None else ini.data_ptr(), ctypes.byref(ccfg), par.data_ptr(),
+                             fl[0].data_ptr(), fl[1].data_ptr(), fl[2].data_ptr(), u8[0].data_ptr(), u8[1].data_ptr(),
+                             ev.data_ptr(), stream))
+            torch.cuda.current_stream(dev).synchronize()
         evs = ev.cpu().tolist()
         return BatchResult(par.cpu().numpy(), fl[0].cpu().numpy(), fl[1].cpu().numpy(), fl[2].cpu().numpy(),
                            u8[0].cpu().numpy(), u8[1].cpu().numpy(),
                            dict(n_gradient_evals=evs[0], n_trial_evals=evs[1], n_kernel_evals=evs[2]))
 
     if inits is None:
-        import torch
-
-        ini = _auto_inits(torch.as_tensor(imgs.astype(np.float32, copy=False)).cuda(), grid, P, config).cpu().numpy()
+        ini = None  # fused initializer: estimated per chunk by the fit kernel, no extra transfer
     else:
         if hasattr(inits, "is_cuda") and inits.is_cuda:  # device inits with host images
             inits = inits.cpu()
@@ -176,9 +178,9 @@ def fit_batch(images, inits=None, config: FitConfig = FitConfig(), engine: str =
     devs = list(devices) if devices else [0]
     dev_arr = (ctypes.c_int32 * len(devs))(*devs)
     entry = L.sf_fit_batch_u16 if imgs.dtype == np.uint16 else L.sf_fit_batch
-    _lib.check(entry(_ptr(imgs), grid.width, grid.height, count, _ptr(ini), ctypes.byref(ccfg),
-                              _ptr(out.params), _ptr(out.alpha), _ptr(out.beta), _ptr(out.nchi2), _ptr(out.status),
-                              _ptr(out.iterations), dev_arr, len(devs), ctypes.byref(st)))
+    _lib.check(entry(_ptr(imgs), grid.width, grid.height, count, None if ini is None else _ptr(ini),
+                     ctypes.byref(ccfg), _ptr(out.params), _ptr(out.alpha), _ptr(out.beta), _ptr(out.nchi2),
+                     _ptr(out.status), _ptr(out.iterations), dev_arr, len(devs), ctypes.byref(st)))
     out.stats = dict(n_gradient_evals=st.n_gradient_evals, n_trial_evals=st.n_trial_evals,
                      n_kernel_evals=st.n_kernel_evals, total_ms=st.total_ms, n_devices=st.n_devices,
                      n_chunks=st.n_chunks)
@@ -189,6 +191,9 @@ def estimate_initial_device(images_cuda, grid: PixelGrid, P: int, config: FitCon
     """GPU initializer on a CUDA tensor (count, N) -> (count, P) [, (count, 2)]."""
     import torch
 
+    if images_cuda.dtype != torch.float32 or not images_cuda.is_cuda:
+        raise TypeError(f"estimate_initial_device takes a float32 CUDA tensor, got {images_cuda.dtype} "
+                        f"on {images_cuda.device}")
     b = config.resolved_bounds(grid)
     count = images_cuda.shape[0]
     ini = torch.empty((count, P), dtype=torch.float32, device=images_cuda.device)

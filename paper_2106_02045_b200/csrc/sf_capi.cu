@@ -96,23 +96,98 @@ void shape_need(const sf::Geom& g, int* ch, int* tl) {
   }
 }
 
+// Work-claim counter slots (sf_fit_kernel.cuh:g_work), per device.  An ordinary
+// launch takes a stream slot whose previous launch has completed (the event
+// recorded behind it has fired); with all kStreamSlots launches still in flight
+// the caller waits for the oldest.  A launch being captured into a CUDA graph
+// takes a graph slot for good (the graph may replay at any time); when those run
+// out the call fails.  Two launches therefore never share a counter, which would
+// split one launch's spots between two grids and leave some unfitted.
+struct WorkPool {
+  std::mutex mu;
+  bool init = false;
+  cudaEvent_t ev[sf::kStreamSlots] = {};
+  bool armed[sf::kStreamSlots] = {};
+  unsigned next = 0;
+  int next_graph = 0;
+  int dev = 0;
+};
+std::mutex g_pool_mu;
+std::vector<std::unique_ptr<WorkPool>> g_pool;
+
+WorkPool* pool_for(int dev) {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if ((int)g_pool.size() <= dev) g_pool.resize(dev + 1);
+  if (!g_pool[dev]) {
+    g_pool[dev].reset(new WorkPool());
+    g_pool[dev]->dev = dev;
+  }
+  return g_pool[dev].get();
+}
+
+// Launches the fit through `launch(slot)` with a private claim counter, under the pool lock.
+template <class Launch>
+int with_work_slot(cudaStream_t st, Launch&& launch) {
+  int dev = 0;
+  SF_CUDA(cudaGetDevice(&dev));
+  WorkPool* w = pool_for(dev);
+  std::lock_guard<std::mutex> lk(w->mu);
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  SF_CUDA(cudaStreamIsCapturing(st, &cs));
+  if (cs == cudaStreamCaptureStatusActive) {
+    if (w->next_graph >= sf::kGraphSlots)
+      return fail("device %d: %d fit launches were already captured into CUDA graphs; each keeps a private "
+                  "work-claim counter and none is left", dev, sf::kGraphSlots);
+    return launch(sf::kStreamSlots + w->next_graph++);
+  }
+  if (cs != cudaStreamCaptureStatusNone) return fail("stream capture was invalidated");
+  if (!w->init) {
+    for (auto& e : w->ev) SF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    w->init = true;
+  }
+  int slot = -1;
+  for (int t = 0; t < sf::kStreamSlots && slot < 0; ++t) {
+    const int k = (int)(w->next++ % (unsigned)sf::kStreamSlots);
+    if (!w->armed[k]) {
+      slot = k;
+      break;
+    }
+    const cudaError_t q = cudaEventQuery(w->ev[k]);
+    if (q == cudaSuccess) {
+      slot = k;
+    } else if (q == cudaErrorNotReady) {
+      (void)cudaGetLastError();  // not an error: the slot's launch is still running
+    } else {
+      return fail("cudaEventQuery failed: %s", cudaGetErrorString(q));
+    }
+  }
+  if (slot < 0) {  // every slot busy: wait for the next one in round-robin order
+    slot = (int)(w->next++ % (unsigned)sf::kStreamSlots);
+    SF_CUDA(cudaEventSynchronize(w->ev[slot]));
+  }
+  if (launch(slot) != 0) return -1;
+  SF_CUDA(cudaEventRecord(w->ev[slot], st));
+  w->armed[slot] = true;
+  return 0;
+}
+
 int dispatch_fit(int P, const sf::LaunchFit& a_in) {
-  // each launch holds one dynamic-claim counter slot (sf_fit_kernel.cuh:g_work) until it ends
-  static std::atomic<unsigned> next_slot{0};
-  sf::LaunchFit a = a_in;
-  a.out.work_slot = (int)(next_slot.fetch_add(1u) % (unsigned)sf::kWorkSlots);
-  cudaError_t err = cudaSuccess;
-  int used = -1;
-  const int slots = a.geom.slots, ch = a.geom.ch, tl = a.geom.tl;
+  return with_work_slot(a_in.stream, [&](int work_slot) -> int {
+    sf::LaunchFit a = a_in;
+    a.out.work_slot = work_slot;
+    cudaError_t err = cudaSuccess;
+    int used = -1;
+    const int slots = a.geom.slots, ch = a.geom.ch, tl = a.geom.tl;
 #define SF_CASE(PP, S) \
   if (P == PP && slots == S) used = sf::launch_fit_P##PP##_S##S(a, &err);
-  SF_CASE(3, 1) SF_CASE(3, 2) SF_CASE(3, 4) SF_CASE(3, 8) SF_CASE(3, 16)
-  SF_CASE(4, 1) SF_CASE(4, 2) SF_CASE(4, 4) SF_CASE(4, 8) SF_CASE(4, 16)
-  SF_CASE(5, 1) SF_CASE(5, 2) SF_CASE(5, 4) SF_CASE(5, 8) SF_CASE(5, 16)
+    SF_CASE(3, 1) SF_CASE(3, 2) SF_CASE(3, 4) SF_CASE(3, 8) SF_CASE(3, 16)
+    SF_CASE(4, 1) SF_CASE(4, 2) SF_CASE(4, 4) SF_CASE(4, 8) SF_CASE(4, 16)
+    SF_CASE(5, 1) SF_CASE(5, 2) SF_CASE(5, 4) SF_CASE(5, 8) SF_CASE(5, 16)
 #undef SF_CASE
-  if (used < 0) return fail("no kernel instantiation for P=%d slots=%d chain=%d tail=%d", P, slots, ch, tl);
-  if (err != cudaSuccess) return fail("fit kernel launch failed: %s", cudaGetErrorString(err));
-  return 0;
+    if (used < 0) return fail("no kernel instantiation for P=%d slots=%d chain=%d tail=%d", P, slots, ch, tl);
+    if (err != cudaSuccess) return fail("fit kernel launch failed: %s", cudaGetErrorString(err));
+    return 0;
+  });
 }
 
 int dispatch_eval(int P, const sf::LaunchEval& a) {
@@ -238,6 +313,28 @@ bool is_pinned_ptr(const void* p) {
   return a.type == cudaMemoryTypeHost;
 }
 
+// Device that owns a device (or managed) allocation, -1 for host memory.
+int owning_device(const void* p) {
+  int d = -1;
+  return (p != nullptr && is_device_ptr(p, &d)) ? d : -1;
+}
+
+// Makes `dev` current for the scope and restores the caller's device afterwards.
+struct DeviceGuard {
+  int prev = -1;
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  cudaError_t set(int dev) {
+    int cur = 0;
+    cudaError_t e = cudaGetDevice(&cur);
+    if (e != cudaSuccess || cur == dev) return e;
+    e = cudaSetDevice(dev);
+    if (e == cudaSuccess) prev = cur;
+    return e;
+  }
+};
+
 struct HostJob {
   const float* images;
   const uint16_t* images16;  // non-null: 16-bit input, widened to f32 on the device
@@ -273,7 +370,8 @@ void copy_out_staged(Slot& s, HostJob& j) {
 }
 
 int run_shard(int dev, HostJob& j) {
-  SF_CUDA(cudaSetDevice(dev));
+  DeviceGuard guard;  // the caller's current device is restored on return
+  SF_CUDA(guard.set(dev));
   DevCtx* c = ctx_for(dev);
   std::lock_guard<std::mutex> lk(c->mu);
   const int N = j.W * j.H, P = j.P;
@@ -337,17 +435,18 @@ int run_shard(int dev, HostJob& j) {
     SF_CUDA(mark(s.stream));
     const size_t px_bytes = j.images16 ? sizeof(uint16_t) : sizeof(float);
     const void* src_img = j.images16 ? (const void*)(j.images16 + lo * N) : (const void*)(j.images + lo * N);
-    const float* src_init = j.inits + lo * P;
+    const float* src_init = j.inits ? j.inits + lo * P : nullptr;  // NULL: the fit kernel estimates them
     if (!j.pinned_in) {
       std::memcpy(s.h_in, src_img, n * N * px_bytes);
-      std::memcpy(s.h_in + s.cap_spots * N, src_init, n * P * sizeof(float));
+      if (src_init) std::memcpy(s.h_in + s.cap_spots * N, src_init, n * P * sizeof(float));
       src_img = s.h_in;
-      src_init = s.h_in + s.cap_spots * N;
+      if (src_init) src_init = s.h_in + s.cap_spots * N;
     }
     // inits first, then pixels: the fit needs nothing else, so it can start (and fill the previous
     // fit's tail) as soon as the copy engine is done.  (A widening kernel between the two copies
     // made the init copy wait behind the next chunks' pixel copies: tools/e2e_trace.py.)
-    SF_CUDA(cudaMemcpyAsync(s.d_init, src_init, n * P * sizeof(float), cudaMemcpyHostToDevice, s.stream));
+    if (src_init)
+      SF_CUDA(cudaMemcpyAsync(s.d_init, src_init, n * P * sizeof(float), cudaMemcpyHostToDevice, s.stream));
     if (j.images16) {
       SF_CUDA(cudaMemcpyAsync(s.d_img16, src_img, n * N * px_bytes, cudaMemcpyHostToDevice, s.stream));
       SF_CUDA(mark(s.stream));
@@ -360,7 +459,7 @@ int run_shard(int dev, HostJob& j) {
     sf::LaunchFit a;
     a.images = s.d_img;
     a.images16 = j.images16 ? s.d_img16 : nullptr;  // staged as u16 by the fit kernel itself
-    a.inits = s.d_init;
+    a.inits = j.inits ? s.d_init : nullptr;  // fused initializer (sf_fit_kernel.cuh:fused_init)
     a.count = n;
     a.geom = geom;
     a.cfg = kc;
@@ -493,9 +592,12 @@ static int fit_device_impl(const float* d_images, const uint16_t* d_images16, in
   sf::Cfg kc;
   if (make_cfg(cfg, width, height, kc) != 0) return -1;
   if (count == 0) return 0;
-  if ((!d_images && !d_images16) || !d_inits || !d_params || !d_alpha || !d_beta || !d_nchi2 || !d_status ||
-      !d_iters)
-    return fail("NULL buffer");
+  if ((!d_images && !d_images16) || !d_params || !d_alpha || !d_beta || !d_nchi2 || !d_status || !d_iters)
+    return fail("NULL buffer");  // d_inits may be NULL: the fit kernel estimates them (fused initializer)
+  // launch on the device that owns the pixels (the current device for device-mapped host memory)
+  DeviceGuard guard;
+  const int owner = owning_device(d_images ? (const void*)d_images : (const void*)d_images16);
+  if (owner >= 0) SF_CUDA(guard.set(owner));
   sf::Geom geom;
   sf::build_geom(width, height, cfg->model, geom);
   sf::LaunchFit a;
@@ -534,6 +636,10 @@ int sf_eval_batch_device(const float* d_images, int32_t width, int32_t height, i
   if (model != 3 && model != 4) return fail("model must be 3 or 4");
   if (count < 0) return fail("negative count");
   if (count == 0) return 0;
+  if (!d_images || !d_params || !d_out) return fail("NULL buffer");
+  DeviceGuard guard;
+  const int owner = owning_device(d_images);
+  if (owner >= 0) SF_CUDA(guard.set(owner));
   sf::Geom geom;
   sf::build_geom(width, height, model, geom);
   sf::LaunchEval a;
@@ -552,6 +658,10 @@ int sf_estimate_initial_device(const float* d_images, int32_t width, int32_t hei
   if (model != 3 && model != 4) return fail("model must be 3 or 4");
   if (count < 0) return fail("negative count");
   if (!(sigma_min > 0) || !(sigma_max > sigma_min)) return fail("need 0 < sigma_min < sigma_max");
+  if (count > 0 && (!d_images || !d_inits)) return fail("NULL buffer");
+  DeviceGuard guard;
+  const int owner = owning_device(d_images);
+  if (owner >= 0) SF_CUDA(guard.set(owner));
   cudaError_t e = sf::launch_estimate_initial(d_images, width, height, count, model, sigma_min, sigma_max, d_inits,
                                               d_amps, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail("initializer launch failed: %s", cudaGetErrorString(e));
@@ -593,9 +703,8 @@ static int fit_batch_impl(const float* images, const uint16_t* images16, int32_t
   if (make_cfg(cfg, width, height, kc) != 0) return -1;
   if (stats) std::memset(stats, 0, sizeof(*stats));
   if (count == 0) return 0;
-  if ((!images && !images16) || !inits || !out_params || !out_alpha || !out_beta || !out_nchi2 || !out_status ||
-      !out_iters)
-    return fail("NULL buffer");
+  if ((!images && !images16) || !out_params || !out_alpha || !out_beta || !out_nchi2 || !out_status || !out_iters)
+    return fail("NULL buffer");  // inits may be NULL: estimated by the fit kernel (fused initializer)
   int ndev_avail = sf_device_count();
   if (ndev_avail < 1) return fail("no CUDA device available (the CUDA engine has no CPU fallback)");
   std::vector<int> devs;
@@ -608,10 +717,20 @@ static int fit_batch_impl(const float* images, const uint16_t* images16, int32_t
     devs.push_back(0);
   }
   int dptr_dev = -1;
+  const void* outs[] = {inits, out_params, out_alpha, out_beta, out_nchi2, out_status, out_iters};
+  const char* names[] = {"inits", "out_params", "out_alpha", "out_beta", "out_nchi2", "out_status", "out_iters"};
   if (images && is_device_ptr(images, &dptr_dev)) {
-    // device-resident batch: one device, synchronous call on the library stream
+    // device-resident batch: one device, synchronous call on the library stream; every other
+    // array must live on the same device (a host output would be written through a device store)
     if (devs.size() > 1) return fail("device-pointer batches run on the owning device only");
-    SF_CUDA(cudaSetDevice(dptr_dev));
+    for (int i = 0; i < 7; ++i) {
+      int d = -1;
+      if (outs[i] == nullptr) continue;  // NULL inits: fused initializer
+      if (!is_device_ptr(outs[i], &d) || d != dptr_dev)
+        return fail("mixed arguments: images are device memory of device %d but %s is not", dptr_dev, names[i]);
+    }
+    DeviceGuard guard;
+    SF_CUDA(guard.set(dptr_dev));
     DevCtx* c = ctx_for(dptr_dev);
     std::lock_guard<std::mutex> lk(c->mu);
     if (ensure_ctx(*c, dptr_dev, 1, width * height, cfg->model, false) != 0) return -1;
@@ -638,7 +757,11 @@ static int fit_batch_impl(const float* images, const uint16_t* images16, int32_t
     }
     return 0;
   }
-  const bool pin_in = is_pinned_ptr(images ? (const void*)images : (const void*)images16) && is_pinned_ptr(inits);
+  for (int i = 0; i < 7; ++i)  // host images: every array is host memory (staged / DMA'd by the pipeline)
+    if (outs[i] != nullptr && is_device_ptr(outs[i], nullptr)) return fail("mixed arguments: images are host memory but %s is device "
+                                                     "memory", names[i]);
+  const bool pin_in =
+      is_pinned_ptr(images ? (const void*)images : (const void*)images16) && (!inits || is_pinned_ptr(inits));
   const bool pin_out = is_pinned_ptr(out_params) && is_pinned_ptr(out_alpha) && is_pinned_ptr(out_beta) &&
                        is_pinned_ptr(out_nchi2) && is_pinned_ptr(out_status) && is_pinned_ptr(out_iters);
   const int nd = (int)devs.size();

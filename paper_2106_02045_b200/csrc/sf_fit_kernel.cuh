@@ -10,6 +10,7 @@
 // happens inside a fit.
 #pragma once
 #include "sf_device.cuh"
+#include "sf_init_core.cuh"
 
 namespace sf {
 
@@ -21,7 +22,7 @@ struct FitOut {
   uint8_t* status;
   uint8_t* iters;
   unsigned long long* evals;  // [3]: reference G-evals, reference T-evals, fused kernel evals (or null)
-  int work_slot;              // g_work slot of this launch (dispatch_fit: round robin)
+  int work_slot;              // g_work slot of this launch (sf_capi.cu:acquire_work_slot)
 };
 
 // Dynamic spot claiming.  Persistent groups take their next spot from a launch-
@@ -30,7 +31,15 @@ struct FitOut {
 // spots (a static stride left ~10% of warp slots idle at the tail: v9 profile,
 // warps_active 14.4 of 16).  g_work[slot] = {next spot, CTAs finished}; the last
 // CTA of a launch resets its slot, so a slot is zero whenever no launch holds it.
-constexpr int kWorkSlots = 256;
+// Slots [0, kStreamSlots) serve ordinary launches: the host (sf_capi.cu:WorkPool)
+// hands a slot out only after the event recorded behind its previous launch has
+// completed, so two launches never share a counter.  Slots [kStreamSlots,
+// kWorkSlots) are owned for good by launches captured into CUDA graphs (replays
+// of one graph exec are serialised by CUDA); when they run out the capture fails
+// with an error instead of sharing.
+constexpr int kStreamSlots = 256;
+constexpr int kGraphSlots = 256;
+constexpr int kWorkSlots = kStreamSlots + kGraphSlots;
 static __device__ unsigned long long g_work[kWorkSlots][2];
 
 // Per-spot LM state, replicated in every lane of the group.  The normal system
@@ -206,6 +215,66 @@ __device__ __forceinline__ bool lm_step(LMState<P>& s, const Eval<P>& E, const C
   return true;
 }
 
+// Fused initializer (inits == NULL): estimate_initial of the spot
+// in the group's staging window, computed by the group's lanes during the refill,
+// so the pixels cross HBM (and, for host batches, PCIe) once.  Same arithmetic as
+// the standalone initializer (sf_init_core.cuh).  Every lane of the warp (CTA when
+// SLOTS >= 8) calls it; lanes with !load only take part in the reductions.
+// Result: (x, y, sigma[, sigma]) -- explicit-5: (x, y, sigma, alpha, beta) as
+// batch_engine._auto_inits builds it.
+template <int P, int SLOTS, typename PX>
+__device__ __forceinline__ void fused_init(const PX* st, bool load, const Geom& geom, const Cfg& cfg, float invW,
+                                           int gl, float (&init)[P]) {
+  constexpr int LANES = 8 * SLOTS;
+  constexpr int LW = LANES < 32 ? LANES : 32;
+  const int N = geom.N, W = geom.W;
+  InitPart p;
+  init_part_reset(p);
+  if (load) init_scan(st, W, geom.H, N, invW, gl, LANES, p);
+#pragma unroll
+  for (int o = 1; o < LW; o <<= 1)
+    init_part_merge(p, __shfl_xor_sync(kFull, p.best, o), __shfl_xor_sync(kFull, p.idx, o),
+                    __shfl_xor_sync(kFull, p.lo, o), __shfl_xor_sync(kFull, p.nan, o));
+  int m = 0;
+  int idx;
+  float alpha, beta;
+  double thr;
+  if constexpr (SLOTS >= 8) {  // the group is the CTA: merge the warps' partials through shared memory
+    constexpr int WARPS = LANES / 32;
+    __shared__ InitPart part[WARPS];
+    __shared__ int msum[WARPS];
+    const int warp = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) part[warp] = p;
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) init_part_merge(p, part[w].best, part[w].idx, part[w].lo, part[w].nan);
+    init_finish(p, idx, alpha, beta, thr);
+    if (load) m = init_count(st, N, thr, gl, LANES);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) m += __shfl_xor_sync(kFull, m, o);
+    if ((threadIdx.x & 31) == 0) msum[warp] = m;
+    __syncthreads();
+    m = 0;
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) m += msum[w];
+    __syncthreads();  // part / msum are rewritten by the next refill
+  } else {
+    init_finish(p, idx, alpha, beta, thr);
+    if (load) m = init_count(st, N, thr, gl, LANES);
+#pragma unroll
+    for (int o = 1; o < LW; o <<= 1) m += __shfl_xor_sync(kFull, m, o);
+  }
+  const float sg = init_sigma(m, cfg.lo[2], cfg.hi[2]);
+  init[0] = (float)(idx % W);
+  init[1] = (float)(idx / W);
+  init[2] = sg;
+  if constexpr (P == 4) init[3] = sg;
+  if constexpr (P == 5) {
+    init[3] = alpha;
+    init[4] = beta;
+  }
+}
+
 // Lane identity and pixel ownership, shared by the fit and eval kernels.
 template <int P, int SLOTS>
 struct LaneSetup {
@@ -316,14 +385,17 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
   // refill waits for the copies, scatters the window into the lanes' pixel
   // slots (load_spot), then starts the following spot's copy.
   float nxt[P];
+  const bool fused = inits == nullptr;  // fused initializer: inits estimated from the staged spot
   int nsh = 0;  // float offset of the staged spot inside its window
   const int gib = L.gib();
   const uintptr_t lo = (uintptr_t)images, hi = (uintptr_t)(images + count * (int64_t)N);
   auto prefetch = [&](int64_t sp) {
     if (sp < count) {
       nsh = stage_spot<P, SLOTS, PX>(S, gib, L.gl, images + sp * (int64_t)N, lo, hi, N);
+      if (!fused) {
 #pragma unroll
-      for (int k = 0; k < P; ++k) nxt[k] = __ldg(inits + sp * P + k);
+        for (int k = 0; k < P; ++k) nxt[k] = __ldg(inits + sp * P + k);
+      }
     }
     cp_async_commit();
   };
@@ -362,6 +434,9 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
       if (load) cp_async_wait_all();  // this lane's copies of `spot` have landed
       group_sync<SLOTS>();             // ... and every other lane's
       bool bad = false;
+      if (fused)
+        fused_init<P, SLOTS, PX>(reinterpret_cast<const PX*>(S.stage + gib * S.sw) + nsh, load, geom, cfg,
+                                 L.lg.invW, L.gl, nxt);
       if (load) {
         float init[P];
         double v[P];
@@ -375,10 +450,10 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
         s.lam = cfg.lam0;
         s.it = 0;
         s.fl = 0u;
-        if (bad) {  // keep the raw init for the InvalidInput result (oracle/lm.py:fit_single)
+        // the raw init is the InvalidInput result (oracle/lm.py:fit_single) whether the init or a
+        // pixel is non-finite; `best` is free until the first G-eval overwrites it
 #pragma unroll
-          for (int k = 0; k < P; ++k) s.p[k] = init[k];
-        }
+        for (int k = 0; k < P; ++k) s.best[k] = init[k];
       }
       // G = sum g (model.py:223); it is non-finite iff some pixel is (a sum of <= 1024 finite
       // f32 values cannot overflow f64), so it doubles as the InvalidInput pixel check
@@ -401,7 +476,7 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
       if (load) {
         G = gsum;
         if (gbad) {
-          write_result<P>(out, spot, leader, s.p, true, 0.f, 0.f, 0.f, N, SF_STOP_NOT_CONVERGED | SF_FLAG_INVALID, 0,
+          write_result<P>(out, spot, leader, s.best, true, 0.f, 0.f, 0.f, N, SF_STOP_NOT_CONVERGED | SF_FLAG_INVALID, 0,
                           S.kc[1]);
           need = true;  // fetch the next spot on the next trip
           skip = true;

@@ -1,100 +1,83 @@
 // sf_init.cu -- GPU initializer: estimate_initial for a whole batch
 // (SURVEY 8f item 1).  One warp per spot.
-//
-// Pinned arithmetic (oracle/initializer.py restates it):
-//   smoothed_i = f32( sum_f64(in-bounds 3x3 neighbours, row-major order) / count )
-//   (x, y)     = coordinates of the first maximum of smoothed (row-major ties)
-//   beta       = min smoothed;  alpha = f32(f64(max) - f64(beta))
-//   M          = #{ i : f64(g_i) > f64(alpha) * exp(-0.5) + f64(beta) }  (original pixels)
-//   sigma      = f32( clamp( sqrt(M / pi), sigma_min, sigma_max ) )
+// The arithmetic is pinned in sf_init_core.cuh (shared with the fit kernel's
+// fused initializer) and restated in oracle/initializer.py.
 #include <cfloat>
 #include <climits>
 
+#include "sf_init_core.cuh"
 #include "sf_launch.h"
 
 namespace sf {
 
 namespace {
-constexpr double kExpMinusHalf = 0x1.368b2fc6f960ap-1;  // exp(-0.5), correctly rounded
-constexpr double kPi = 3.141592653589793115997963468544185161590576171875;
 
-// One warp per spot; the spot is staged in shared memory with coalesced loads (the 3x3 means
-// read it 9x), and pixel coordinates come from the exact float reciprocal (idx + 0.5) / W
-// instead of integer division.  Arithmetic exactly as pinned above.
+// Standalone initializer: one warp per spot, persistent over spots.  Each spot is
+// widened once into a zero-padded (W+2) x (H+2) f64 tile in shared memory, so the
+// 3x3 window needs no bounds checks and no per-tap conversion: the padding adds
+// +0.0, which leaves every partial sum unchanged (a sum that starts at +0.0 is
+// never -0.0), so the row-major f64 sum is sf_init_core.cuh's bit for bit.  The
+// in-bounds count is (1 + [x>0] + [x<W-1]) (1 + [y>0] + [y<H-1]).
 constexpr int kInitWarps = 8;
 __global__ void __launch_bounds__(32 * kInitWarps) init_kernel(const float* __restrict__ images, int W, int H,
                                                               int64_t count, int P, double smin, double smax,
                                                               float* __restrict__ inits, float* __restrict__ amps) {
-  extern __shared__ float init_smem[];  // [kInitWarps][N]
+  extern __shared__ double init_tile[];  // [kInitWarps][(W + 2) * (H + 2)]
   const int warp = threadIdx.x >> 5;
-  const int64_t spot = (int64_t)blockIdx.x * kInitWarps + warp;
   const int lane = threadIdx.x & 31;
-  if (spot >= count) return;
-  const int N = W * H;
-  float* sg = init_smem + warp * N;
-  const float* g = images + spot * (int64_t)N;
-  for (int i = lane; i < N; i += 32) sg[i] = __ldg(g + i);
-  __syncwarp();
-  const float Wf = (float)W, invW = 1.0f / Wf;
-  float best = -INFINITY, lo = INFINITY;
-  int bidx = INT_MAX;
-  for (int i = lane; i < N; i += 32) {
-    // y = floor((i + 0.5) / W) exactly (small integers, never a tie), x = i - y W
-    const int y = (int)(((float)i + 0.5f) * invW);
-    const int x = i - y * W;
-    double s = 0.0;
-    int cnt = 0;
-#pragma unroll
-    for (int dy = -1; dy <= 1; ++dy) {
-      const int yy = y + dy;
-      const bool vy = yy >= 0 && yy < H;
-#pragma unroll
-      for (int dx = -1; dx <= 1; ++dx) {
-        const int xx = x + dx;
-        const bool v = vy && xx >= 0 && xx < W;
-        const float val = v ? sg[yy * W + xx] : 0.0f;
-        if (v) {
-          s = s + (double)val;
-          ++cnt;
-        }
-      }
+  const int N = W * H, PW = W + 2, PN = (W + 2) * (H + 2);
+  double* t = init_tile + warp * PN;
+  for (int i = lane; i < PN; i += 32) t[i] = 0.0;  // borders stay +0.0; the interior is rewritten per spot
+  const float invW = 1.0f / (float)W;
+  const int64_t stride = (int64_t)gridDim.x * kInitWarps;
+#pragma unroll 1
+  for (int64_t spot = (int64_t)blockIdx.x * kInitWarps + warp; spot < count; spot += stride) {
+    const float* g = images + spot * (int64_t)N;
+    __syncwarp();  // the previous spot's tile reads are done
+#pragma unroll 4
+    for (int i = lane; i < N; i += 32) {
+      const int y = (int)(((float)i + 0.5f) * invW);
+      t[(y + 1) * PW + (i - y * W) + 1] = (double)__ldcs(g + i);
     }
-    const float v = (float)(s / (double)cnt);
-    if (v > best || (v == best && i < bidx)) {
-      best = v;
-      bidx = i;
-    }
-    lo = fminf(lo, v);
-  }
+    __syncwarp();
+    InitPart p;
+    init_part_reset(p);
+#pragma unroll 2
+    for (int i = lane; i < N; i += 32) {
+      const int y = (int)(((float)i + 0.5f) * invW);
+      const int x = i - y * W;
+      const double* c = t + y * PW + x;  // top-left of the padded window
+      double s = 0.0;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const float ob = __shfl_xor_sync(0xffffffffu, best, o);
-    const int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
-    if (ob > best || (ob == best && oi < bidx)) {
-      best = ob;
-      bidx = oi;
-    }
-    lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-  }
-  if (bidx == INT_MAX) bidx = 0;
-  const float alpha = (float)((double)best - (double)lo);
-  const double thr = (double)alpha * kExpMinusHalf + (double)lo;
-  int m = 0;
-  for (int i = lane; i < N; i += 32) m += ((double)sg[i] > thr) ? 1 : 0;
+      for (int dy = 0; dy < 3; ++dy)
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
-  double sgm = sqrt((double)m / kPi);
-  sgm = sgm < smin ? smin : (sgm > smax ? smax : sgm);
-  if (lane == 0) {
-    float* o = inits + spot * P;
-    o[0] = (float)(bidx % W);
-    o[1] = (float)(bidx / W);
-    o[2] = (float)sgm;
-    if (P == 4) o[3] = (float)sgm;
-    if (amps != nullptr) {
-      amps[2 * spot] = alpha;
-      amps[2 * spot + 1] = lo;
+        for (int dx = 0; dx < 3; ++dx) s = __dadd_rn(s, c[dy * PW + dx]);
+      const int cnt = (1 + (x > 0) + (x < W - 1)) * (1 + (y > 0) + (y < H - 1));
+      const float v = (float)(s / (double)cnt);
+      if (v != v) p.nan |= i == 0 ? 3 : 1;
+      init_part_merge(p, v, i, v, 0);
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+      init_part_merge(p, __shfl_xor_sync(kFull, p.best, o), __shfl_xor_sync(kFull, p.idx, o),
+                      __shfl_xor_sync(kFull, p.lo, o), __shfl_xor_sync(kFull, p.nan, o));
+    int idx;
+    float alpha, beta;
+    double thr;
+    init_finish(p, idx, alpha, beta, thr);
+    int m = 0;
+    for (int i = lane; i < N; i += 32) {
+      const int y = (int)(((float)i + 0.5f) * invW);
+      m += (t[(y + 1) * PW + (i - y * W) + 1] > thr) ? 1 : 0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m += __shfl_xor_sync(kFull, m, o);
+    const float sg = init_sigma(m, smin, smax);
+    if (lane < P) {
+      const float v = lane == 0 ? (float)(idx % W) : (lane == 1 ? (float)(idx / W) : sg);
+      inits[spot * P + lane] = v;
+    }
+    if (amps != nullptr && lane < 2) amps[2 * spot + lane] = lane == 0 ? alpha : beta;
   }
 }
 }  // namespace
@@ -102,8 +85,17 @@ __global__ void __launch_bounds__(32 * kInitWarps) init_kernel(const float* __re
 cudaError_t launch_estimate_initial(const float* images, int W, int H, int64_t count, int P, double sigma_min,
                                     double sigma_max, float* inits, float* amps, cudaStream_t stream) {
   if (count <= 0) return cudaSuccess;
-  const int64_t blocks = (count + kInitWarps - 1) / kInitWarps;
-  const size_t smem = (size_t)kInitWarps * W * H * sizeof(float);  // <= 32 KB (N <= 1024)
+  const size_t smem = (size_t)kInitWarps * (W + 2) * (H + 2) * sizeof(double);  // <= 66 KB (N <= 1024)
+  cudaError_t e = cudaFuncSetAttribute(init_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 0, per_sm = 0;
+  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+  if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, init_kernel, 32 * kInitWarps, smem)) != cudaSuccess)
+    return e;
+  int64_t blocks = (int64_t)(per_sm > 0 ? per_sm : 1) * sms;
+  const int64_t need = (count + kInitWarps - 1) / kInitWarps;
+  if (blocks > need) blocks = need;
   init_kernel<<<(unsigned)blocks, 32 * kInitWarps, smem, stream>>>(images, W, H, count, P, sigma_min, sigma_max,
                                                                    inits, amps);
   return cudaGetLastError();

@@ -22,7 +22,10 @@ def estimate_initial_batch(images, model: int = 3, config: FitConfig = FitConfig
 
     _lib.require_gpu()
     imgs, grid = _as_image_array(images, grid)
-    t = imgs if isinstance(imgs, torch.Tensor) else torch.as_tensor(imgs).cuda()
+    # the initializer kernel reads float32 pixels: u16 counts (kept as u16 by _as_image_array for the
+    # fit path) are widened exactly first
+    t = imgs if isinstance(imgs, torch.Tensor) else torch.as_tensor(np.asarray(imgs, dtype=np.float32)).cuda()
+    t = t.float().contiguous()
     ini, am = estimate_initial_device(t, grid, model, config, amps=True)
     torch.cuda.current_stream().synchronize()
     return ini.cpu().numpy(), am.cpu().numpy()
