@@ -154,6 +154,39 @@ int sf_eval_batch_device(const float* d_images, int32_t width, int32_t height, i
                          const float* d_params, sf_eval_record* d_out, void* stream);
 
 /*
+ * spotfit.model function surface (pkg/src/spotfit/model.py:168-315), batched:
+ * each entry point replaces one reference function and takes / returns the
+ * per-pixel arrays that function does, so a caller can chain them as model.py
+ * does (also on f / fgrad arrays that did not come from the profile).  All
+ * pointers are device-accessible memory; asynchronous on `stream`.  n = pixels
+ * per spot (1..1024); model 3 (x, y, sigma) or 4 (x, y, sigma_x, sigma_y) sets
+ * the column count P of fgrad / dmat / gradient arrays.  Bit-identical to the
+ * reference (f32 per-pixel ops, numpy float32 exp, numpy-order f64 sums).
+ */
+/* profile (model.py:168-177) / profile_and_gradient (180-199): params [count][P];
+ * f [count][n]; fgrad [count][n][P] or NULL. */
+int sf_model_profile_device(const float* d_params, int32_t width, int32_t height, int64_t count, int32_t model,
+                            float* d_f, float* d_fgrad, void* stream);
+/* alpha_beta (model.py:207-234): f, g [count][n] -> alpha, beta [count] (f32-quantised,
+ * NaN where SingularProfile is raised), sums [count][5] = (F, G, FF, FG, denom), singular [count]. */
+int sf_model_alpha_beta_device(const float* d_f, const float* d_g, int32_t n, int64_t count, float* d_alpha,
+                               float* d_beta, double* d_sums, int32_t* d_singular, void* stream);
+/* model_values (237-239), residuals (242-244), chi_squared (247-250): h, r [count][n] or NULL; chi [count]. */
+int sf_model_chi_squared_device(const float* d_g, const float* d_f, const float* d_alpha, const float* d_beta,
+                                int32_t n, int64_t count, float* d_h, float* d_r, float* d_chi, void* stream);
+/* gradient_sums (253-267): gsums [count][4][P] = df, dff, dfg, gamma. */
+int sf_model_gradient_sums_device(const float* d_f, const float* d_fgrad, const float* d_g, const double* d_sums,
+                                  int32_t n, int32_t model, int64_t count, double* d_gsums, void* stream);
+/* coefficient_gradients (270-288): dalpha, dbeta [count][P] (NaN + singular where the reference raises). */
+int sf_model_coefficient_gradients_device(const double* d_sums, const double* d_gsums, const float* d_alpha,
+                                          const float* d_beta, int32_t n, int32_t model, int64_t count,
+                                          double* d_dalpha, double* d_dbeta, int32_t* d_singular, void* stream);
+/* chi_gradient (291-315): grad [count][P] f64, dmat [count][n][P] f32 or NULL. */
+int sf_model_chi_gradient_device(const float* d_g, const float* d_f, const float* d_fgrad, const float* d_alpha,
+                                 const float* d_beta, const double* d_dalpha, const double* d_dbeta, int32_t n,
+                                 int32_t model, int64_t count, double* d_grad, float* d_dmat, void* stream);
+
+/*
  * sf_estimate_initial_device -- replaces estimate_initial (SPEC.md:286-290,
  * PAPER.md:212) for a whole batch on the GPU: 3x3 truncated moving average,
  * argmax -> centre, min -> beta, max-beta -> alpha, sigma = sqrt(M/pi) clamped.
@@ -219,6 +252,13 @@ int sf_debug_npexp_device(const float* d_x, float* d_y, int64_t n, int32_t varia
  * model.py:226-233, 281-287) on device arrays; must equal IEEE a / b.
  */
 int sf_debug_ddiv_device(const double* d_a, const double* d_b, double* d_out, int64_t n, void* stream);
+
+/*
+ * sf_debug_tame_div_device -- diagnostic: counts (into *d_mismatches, device u64, accumulated)
+ * the integers s in [0, 9 * 2^20] and window counts c in {1, 2, 3, 4, 6, 9} for which the
+ * initializer's integer-path division (sf_init_core.cuh:tame_div) differs from IEEE s / c.
+ */
+int sf_debug_tame_div_device(uint64_t* d_mismatches, void* stream);
 
 int sf_device_count(void);
 const char* sf_last_error(void);

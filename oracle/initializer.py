@@ -64,3 +64,43 @@ def estimate_initial_batch(images: np.ndarray, W: int, H: int, sigma_min: float,
         p, a, b = estimate_initial(images[s].reshape(H, W), sigma_min, sigma_max, model)
         out[s], amps[s] = p, (a, b)
     return out, amps
+
+
+def estimate_initial_batch_np(images: np.ndarray, W: int, H: int, sigma_min: float, sigma_max: float,
+                              model: int = 3):
+    """estimate_initial_batch vectorised over spots (same results, bit for bit): the 3x3 sums run
+    over a zero-padded f64 copy in the same row-major neighbour order (a +0.0 pad leaves every
+    partial sum unchanged, since a sum starting at +0.0 is never -0.0).  Rows holding a
+    non-finite pixel go through the scalar loop (numpy's argmax treats NaN differently from the
+    strict ">" scan)."""
+    count = images.shape[0]
+    g = np.asarray(images, np.float32).reshape(count, H, W)
+    pad = np.zeros((count, H + 2, W + 2), np.float64)
+    pad[:, 1:-1, 1:-1] = g
+    s = np.zeros((count, H, W), np.float64)
+    for dy in range(3):
+        for dx in range(3):
+            s = s + pad[:, dy:dy + H, dx:dx + W]
+    cy = 1 + (np.arange(H) > 0) + (np.arange(H) < H - 1)
+    cx = 1 + (np.arange(W) > 0) + (np.arange(W) < W - 1)
+    sm = (s / (cy[:, None] * cx[None, :]).astype(np.float64)).astype(np.float32).reshape(count, -1)
+    idx = np.argmax(sm, axis=1)  # first maximum (finite rows)
+    best = sm[np.arange(count), idx].astype(np.float64)
+    lo = sm.min(axis=1).astype(np.float64)
+    alpha = (best - lo).astype(np.float32)
+    thr = alpha.astype(np.float64) * EXP_MINUS_HALF + lo
+    M = np.sum(g.reshape(count, -1).astype(np.float64) > thr[:, None], axis=1)
+    sg = np.sqrt(M / math.pi)
+    sg = np.where(sg < sigma_min, sigma_min, np.where(sg > sigma_max, sigma_max, sg)).astype(np.float32)
+    out = np.empty((count, model), np.float32)
+    out[:, 0] = (idx % W).astype(np.float32)
+    out[:, 1] = (idx // W).astype(np.float32)
+    out[:, 2] = sg
+    if model == 4:
+        out[:, 3] = sg
+    amps = np.stack([alpha, lo.astype(np.float32)], axis=1)
+    bad = ~np.all(np.isfinite(g.reshape(count, -1)), axis=1)
+    for r in np.nonzero(bad)[0]:
+        p, a, b = estimate_initial(g[r], sigma_min, sigma_max, model)
+        out[r], amps[r] = p, (a, b)
+    return out, amps

@@ -104,11 +104,20 @@ SYMBOLS = {
                                                _vp, _vp, _vp, _vp, _vp]),
     "sf_eval_batch_device": (ctypes.c_int, [_vp, _i32, _i32, _i64, _i32, _vp, _vp, _vp]),
     "sf_estimate_initial_device": (ctypes.c_int, [_vp, _i32, _i32, _i64, _i32, _f64, _f64, _vp, _vp, _vp]),
+    "sf_model_profile_device": (ctypes.c_int, [_vp, _i32, _i32, _i64, _i32, _vp, _vp, _vp]),
+    "sf_model_alpha_beta_device": (ctypes.c_int, [_vp, _vp, _i32, _i64, _vp, _vp, _vp, _vp, _vp]),
+    "sf_model_chi_squared_device": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i32, _i64, _vp, _vp, _vp, _vp]),
+    "sf_model_gradient_sums_device": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i32, _i32, _i64, _vp, _vp]),
+    "sf_model_coefficient_gradients_device": (ctypes.c_int, [_vp, _vp, _vp, _vp, _i32, _i32, _i64, _vp, _vp, _vp,
+                                                             _vp]),
+    "sf_model_chi_gradient_device": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i64, _vp, _vp,
+                                                    _vp]),
     "sf_simulate_host": (ctypes.c_int, [ctypes.POINTER(sf_sim_config), _i32, _i32, _i64, _i64, _vp, _vp, _i32]),
     "sf_simulate_device": (ctypes.c_int, [ctypes.POINTER(sf_sim_config), _i32, _i32, _i64, _i64, _vp, _vp, _vp]),
     "sf_lane_geometry": (ctypes.c_int, [_i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp]),
     "sf_debug_npexp_device": (ctypes.c_int, [_vp, _vp, _i64, _i32, _vp]),
     "sf_debug_ddiv_device": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp]),
+    "sf_debug_tame_div_device": (ctypes.c_int, [_vp, _vp]),
     "sf_host_alloc": (ctypes.c_void_p, [ctypes.c_size_t]),
     "sf_host_free": (None, [_vp]),
     "sf_device_count": (ctypes.c_int, []),

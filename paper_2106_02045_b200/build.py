@@ -70,7 +70,7 @@ def build(force: bool = False, jobs: int = 0, verbose: bool = False, variant: st
         out = os.path.join(obj, f"sf_inst_P{p}_S{s}.o")
         cmd = [nvcc()] + NVCC_FLAGS + dflags + [f"-DSF_P={p}", f"-DSF_SLOTS={s}", "-c", src, "-o", out]
         tasks.append((out, [src] + hdrs, cmd))
-    for name in ("sf_init.cu", "sf_capi.cu", "sf_sim.cu"):
+    for name in ("sf_init.cu", "sf_capi.cu", "sf_sim.cu", "sf_model.cu"):
         src = os.path.join(CSRC, name)
         out = os.path.join(obj, name.replace(".cu", ".o"))
         tasks.append((out, [src] + hdrs, [nvcc()] + NVCC_FLAGS + dflags + ["-c", src, "-o", out]))

@@ -459,7 +459,19 @@ int run_shard(int dev, HostJob& j) {
     sf::LaunchFit a;
     a.images = s.d_img;
     a.images16 = j.images16 ? s.d_img16 : nullptr;  // staged as u16 by the fit kernel itself
-    a.inits = j.inits ? s.d_init : nullptr;  // fused initializer (sf_fit_kernel.cuh:fused_init)
+    a.inits = s.d_init;
+    if (!j.inits) {  // no inits: estimate them on the device from the chunk just copied
+      if (n <= sf::kFusedInitMaxSpots) {
+        a.inits = nullptr;  // the fit kernel's fused initializer
+      } else {
+        // P = 5: (x, y, sigma, alpha, beta), as batch_engine._auto_inits builds it
+        const cudaError_t e = j.images16 ? sf::launch_estimate_initial_u16(s.d_img16, j.W, j.H, n, P, kc.lo[2],
+                                                                           kc.hi[2], s.d_init, nullptr, s.stream)
+                                         : sf::launch_estimate_initial(s.d_img, j.W, j.H, n, P, kc.lo[2], kc.hi[2],
+                                                                       s.d_init, nullptr, s.stream);
+        if (e != cudaSuccess) return fail("initializer launch failed: %s", cudaGetErrorString(e));
+      }
+    }
     a.count = n;
     a.geom = geom;
     a.cfg = kc;
@@ -542,6 +554,14 @@ int sf_debug_ddiv_device(const double* d_a, const double* d_b, double* d_out, in
   return 0;
 }
 
+int sf_debug_tame_div_device(uint64_t* d_mismatches, void* stream) {
+  if (!d_mismatches) return fail("NULL buffer");
+  cudaError_t e = sf::launch_tame_div(reinterpret_cast<unsigned long long*>(d_mismatches),
+                                      static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail("tame_div launch failed: %s", cudaGetErrorString(e));
+  return 0;
+}
+
 int sf_lane_geometry(int32_t width, int32_t height, int32_t* slots, int32_t* ppl, int16_t* nc, int16_t* nt,
                      int16_t* base, int16_t* tbase) {
   if (check_grid(width, height) != 0) return -1;
@@ -611,7 +631,26 @@ static int fit_device_impl(const float* d_images, const uint16_t* d_images16, in
                      reinterpret_cast<unsigned long long*>(d_evals)};
   a.stream = static_cast<cudaStream_t>(stream);
   a.sm_count = sm_count_of_current();
-  return dispatch_fit(cfg->model, a);
+  float* tmp = nullptr;
+  if (!d_inits && count > sf::kFusedInitMaxSpots) {
+    // large batch without inits: the standalone initializer into a stream-ordered scratch buffer
+    // in front of the fit (the fused initializer is the small-batch / latency path)
+    const int P = cfg->model;
+    SF_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tmp), (size_t)count * P * sizeof(float), a.stream));
+    const cudaError_t e = d_images16
+                              ? sf::launch_estimate_initial_u16(d_images16, width, height, count, P, kc.lo[2],
+                                                                kc.hi[2], tmp, nullptr, a.stream)
+                              : sf::launch_estimate_initial(d_images, width, height, count, P, kc.lo[2], kc.hi[2],
+                                                            tmp, nullptr, a.stream);
+    if (e != cudaSuccess) {
+      cudaFreeAsync(tmp, a.stream);
+      return fail("initializer launch failed: %s", cudaGetErrorString(e));
+    }
+    a.inits = tmp;
+  }
+  const int rc = dispatch_fit(cfg->model, a);
+  if (tmp) SF_CUDA(cudaFreeAsync(tmp, a.stream));
+  return rc;
 }
 
 int sf_fit_batch_device(const float* d_images, int32_t width, int32_t height, int64_t count, const float* d_inits,
@@ -650,6 +689,90 @@ int sf_eval_batch_device(const float* d_images, int32_t width, int32_t height, i
   a.out = d_out;
   a.stream = static_cast<cudaStream_t>(stream);
   return dispatch_eval(model, a);
+}
+
+static int model_args(int n, int model, int64_t count) {
+  if (n < 1 || n > 1024) return fail("n = %d pixels per spot: need 1..1024 (model.py:55-58)", n);
+  if (model != 3 && model != 4) return fail("model must be 3 or 4");
+  if (count < 0) return fail("negative count");
+  return 0;
+}
+
+#define SF_LAUNCHED(call)                                                            \
+  do {                                                                               \
+    const cudaError_t e_ = (call);                                                   \
+    if (e_ != cudaSuccess) return fail("%s: %s", #call, cudaGetErrorString(e_));     \
+    return 0;                                                                        \
+  } while (0)
+
+int sf_model_profile_device(const float* d_params, int32_t width, int32_t height, int64_t count, int32_t model,
+                            float* d_f, float* d_fgrad, void* stream) {
+  if (check_grid(width, height) != 0 || model_args(width * height, model, count) != 0) return -1;
+  if (count > 0 && (!d_params || !d_f)) return fail("NULL buffer");
+  DeviceGuard guard;
+  const int owner = owning_device(d_params);
+  if (owner >= 0) SF_CUDA(guard.set(owner));
+  SF_LAUNCHED(sf::launch_model_profile(d_params, width, height, count, model, d_f, d_fgrad,
+                                       static_cast<cudaStream_t>(stream)));
+}
+
+int sf_model_alpha_beta_device(const float* d_f, const float* d_g, int32_t n, int64_t count, float* d_alpha,
+                               float* d_beta, double* d_sums, int32_t* d_singular, void* stream) {
+  if (model_args(n, 3, count) != 0) return -1;
+  if (count > 0 && (!d_f || !d_g || !d_alpha || !d_beta || !d_sums || !d_singular)) return fail("NULL buffer");
+  DeviceGuard guard;
+  const int owner = owning_device(d_f);
+  if (owner >= 0) SF_CUDA(guard.set(owner));
+  SF_LAUNCHED(sf::launch_model_alpha_beta(d_f, d_g, n, count, d_alpha, d_beta, d_sums, d_singular,
+                                          static_cast<cudaStream_t>(stream)));
+}
+
+int sf_model_chi_squared_device(const float* d_g, const float* d_f, const float* d_alpha, const float* d_beta,
+                                int32_t n, int64_t count, float* d_h, float* d_r, float* d_chi, void* stream) {
+  if (model_args(n, 3, count) != 0) return -1;
+  if (count > 0 && (!d_g || !d_f || !d_alpha || !d_beta || !d_chi)) return fail("NULL buffer");
+  DeviceGuard guard;
+  const int owner = owning_device(d_f);
+  if (owner >= 0) SF_CUDA(guard.set(owner));
+  SF_LAUNCHED(sf::launch_model_chi(d_g, d_f, d_alpha, d_beta, n, count, d_h, d_r, d_chi,
+                                   static_cast<cudaStream_t>(stream)));
+}
+
+int sf_model_gradient_sums_device(const float* d_f, const float* d_fgrad, const float* d_g, const double* d_sums,
+                                  int32_t n, int32_t model, int64_t count, double* d_gsums, void* stream) {
+  if (model_args(n, model, count) != 0) return -1;
+  if (count > 0 && (!d_f || !d_fgrad || !d_g || !d_sums || !d_gsums)) return fail("NULL buffer");
+  DeviceGuard guard;
+  const int owner = owning_device(d_f);
+  if (owner >= 0) SF_CUDA(guard.set(owner));
+  SF_LAUNCHED(sf::launch_model_gradient_sums(d_f, d_fgrad, d_g, d_sums, n, model, count, d_gsums,
+                                             static_cast<cudaStream_t>(stream)));
+}
+
+int sf_model_coefficient_gradients_device(const double* d_sums, const double* d_gsums, const float* d_alpha,
+                                          const float* d_beta, int32_t n, int32_t model, int64_t count,
+                                          double* d_dalpha, double* d_dbeta, int32_t* d_singular, void* stream) {
+  if (model_args(n, model, count) != 0) return -1;
+  if (count > 0 && (!d_sums || !d_gsums || !d_alpha || !d_beta || !d_dalpha || !d_dbeta || !d_singular))
+    return fail("NULL buffer");
+  DeviceGuard guard;
+  const int owner = owning_device(d_sums);
+  if (owner >= 0) SF_CUDA(guard.set(owner));
+  SF_LAUNCHED(sf::launch_model_coefficient_gradients(d_sums, d_gsums, d_alpha, d_beta, n, model, count, d_dalpha,
+                                                     d_dbeta, d_singular, static_cast<cudaStream_t>(stream)));
+}
+
+int sf_model_chi_gradient_device(const float* d_g, const float* d_f, const float* d_fgrad, const float* d_alpha,
+                                 const float* d_beta, const double* d_dalpha, const double* d_dbeta, int32_t n,
+                                 int32_t model, int64_t count, double* d_grad, float* d_dmat, void* stream) {
+  if (model_args(n, model, count) != 0) return -1;
+  if (count > 0 && (!d_g || !d_f || !d_fgrad || !d_alpha || !d_beta || !d_dalpha || !d_dbeta || !d_grad))
+    return fail("NULL buffer");
+  DeviceGuard guard;
+  const int owner = owning_device(d_f);
+  if (owner >= 0) SF_CUDA(guard.set(owner));
+  SF_LAUNCHED(sf::launch_model_chi_gradient(d_g, d_f, d_fgrad, d_alpha, d_beta, d_dalpha, d_dbeta, n, model, count,
+                                            d_grad, d_dmat, static_cast<cudaStream_t>(stream)));
 }
 
 int sf_estimate_initial_device(const float* d_images, int32_t width, int32_t height, int64_t count, int32_t model,

@@ -216,57 +216,87 @@ __device__ __forceinline__ bool lm_step(LMState<P>& s, const Eval<P>& E, const C
 }
 
 // Fused initializer (inits == NULL): estimate_initial of the spot
-// in the group's staging window, computed by the group's lanes during the refill,
-// so the pixels cross HBM (and, for host batches, PCIe) once.  Same arithmetic as
-// the standalone initializer (sf_init_core.cuh).  Every lane of the warp (CTA when
+// in the group's staging window, computed during the refill, so the pixels cross
+// HBM (and, for host batches, PCIe) once.  Same arithmetic as the standalone
+// initializer (sf_init_core.cuh); tame: every pixel of the spot is an integer in
+// [0, 2^20] (load_spot), which takes the exact integer column walk.  When exactly
+// one group of a multi-group warp refills -- the common case -- the whole warp
+// scans its spot (the other groups' lanes would idle through the refill anyway),
+// else each refilling group scans its own.  Every lane of the warp (CTA when
 // SLOTS >= 8) calls it; lanes with !load only take part in the reductions.
 // Result: (x, y, sigma[, sigma]) -- explicit-5: (x, y, sigma, alpha, beta) as
 // batch_engine._auto_inits builds it.
 template <int P, int SLOTS, typename PX>
-__device__ __forceinline__ void fused_init(const PX* st, bool load, const Geom& geom, const Cfg& cfg, float invW,
-                                           int gl, float (&init)[P]) {
+__device__ __forceinline__ void fused_init(const PX* st, bool load, bool tame, const Geom& geom, const Cfg& cfg,
+                                           float invW, int gl, float (&init)[P]) {
   constexpr int LANES = 8 * SLOTS;
   constexpr int LW = LANES < 32 ? LANES : 32;
-  const int N = geom.N, W = geom.W;
-  InitPart p;
-  init_part_reset(p);
-  if (load) init_scan(st, W, geom.H, N, invW, gl, LANES, p);
-#pragma unroll
-  for (int o = 1; o < LW; o <<= 1)
-    init_part_merge(p, __shfl_xor_sync(kFull, p.best, o), __shfl_xor_sync(kFull, p.idx, o),
-                    __shfl_xor_sync(kFull, p.lo, o), __shfl_xor_sync(kFull, p.nan, o));
+  const int N = geom.N, W = geom.W, H = geom.H;
   int m = 0;
   int idx;
   float alpha, beta;
   double thr;
-  if constexpr (SLOTS >= 8) {  // the group is the CTA: merge the warps' partials through shared memory
-    constexpr int WARPS = LANES / 32;
-    __shared__ InitPart part[WARPS];
-    __shared__ int msum[WARPS];
-    const int warp = threadIdx.x >> 5;
-    if ((threadIdx.x & 31) == 0) part[warp] = p;
-    __syncthreads();
+  bool done = false;
+  if constexpr (LANES < 32) {
+    const unsigned lm = __ballot_sync(kFull, load);
+    if (__popc(lm) == LANES) {  // warp-uniform: one group refills, all 32 lanes scan its window
+      const int src = __ffs(lm) - 1, lane = threadIdx.x & 31;
+      const PX* wst = reinterpret_cast<const PX*>(__shfl_sync(kFull, reinterpret_cast<unsigned long long>(st), src));
+      const bool wtame = __shfl_sync(kFull, tame ? 1 : 0, src) != 0;
+      InitScan a;
+      scan_reset(a);
+      if (wtame)
+        init_scan_tame<32, PX>(wst, W, H, lane, a);
+      else
+        init_scan(wst, W, H, N, invW, lane, 32, a);
+      scan_reduce<32>(a);
+      init_finish(a, idx, alpha, beta, thr);
+      m = wtame ? init_count_tame(wst, N, thr, lane, 32) : init_count(wst, N, thr, lane, 32);
 #pragma unroll
-    for (int w = 0; w < WARPS; ++w) init_part_merge(p, part[w].best, part[w].idx, part[w].lo, part[w].nan);
-    init_finish(p, idx, alpha, beta, thr);
-    if (load) m = init_count(st, N, thr, gl, LANES);
+      for (int o = 1; o < 32; o <<= 1) m += __shfl_xor_sync(kFull, m, o);
+      done = true;
+    }
+  }
+  if (!done) {
+    InitScan a;
+    scan_reset(a);
+    if (load) {  // tame is group-uniform (it may differ between the groups of a warp): no shuffles inside
+      if (tame)
+        init_scan_tame<LANES, PX>(st, W, H, gl, a);
+      else
+        init_scan(st, W, H, N, invW, gl, LANES, a);
+    }
+    scan_reduce<LW>(a);
+    if constexpr (SLOTS >= 8) {  // the group is the CTA: merge the warps' partials through shared memory
+      constexpr int WARPS = LANES / 32;
+      __shared__ InitScan part[WARPS];
+      __shared__ int msum[WARPS];
+      const int warp = threadIdx.x >> 5;
+      if ((threadIdx.x & 31) == 0) part[warp] = a;
+      __syncthreads();
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) m += __shfl_xor_sync(kFull, m, o);
-    if ((threadIdx.x & 31) == 0) msum[warp] = m;
-    __syncthreads();
-    m = 0;
+      for (int w = 0; w < WARPS; ++w) scan_merge(a, part[w].key, part[w].lo, part[w].nan);
+      init_finish(a, idx, alpha, beta, thr);
+      if (load) m = tame ? init_count_tame(st, N, thr, gl, LANES) : init_count(st, N, thr, gl, LANES);
 #pragma unroll
-    for (int w = 0; w < WARPS; ++w) m += msum[w];
-    __syncthreads();  // part / msum are rewritten by the next refill
-  } else {
-    init_finish(p, idx, alpha, beta, thr);
-    if (load) m = init_count(st, N, thr, gl, LANES);
+      for (int o = 1; o < 32; o <<= 1) m += __shfl_xor_sync(kFull, m, o);
+      if ((threadIdx.x & 31) == 0) msum[warp] = m;
+      __syncthreads();
+      m = 0;
 #pragma unroll
-    for (int o = 1; o < LW; o <<= 1) m += __shfl_xor_sync(kFull, m, o);
+      for (int w = 0; w < WARPS; ++w) m += msum[w];
+      __syncthreads();  // part / msum are rewritten by the next refill
+    } else {
+      init_finish(a, idx, alpha, beta, thr);
+      if (load) m = tame ? init_count_tame(st, N, thr, gl, LANES) : init_count(st, N, thr, gl, LANES);
+#pragma unroll
+      for (int o = 1; o < LW; o <<= 1) m += __shfl_xor_sync(kFull, m, o);
+    }
   }
   const float sg = init_sigma(m, cfg.lo[2], cfg.hi[2]);
-  init[0] = (float)(idx % W);
-  init[1] = (float)(idx / W);
+  const int iy = (int)(((float)idx + 0.5f) * invW);  // idx / W exactly (sf_init_core.cuh:init_smoothed)
+  init[0] = (float)(idx - iy * W);
+  init[1] = (float)iy;
   init[2] = sg;
   if constexpr (P == 4) init[3] = sg;
   if constexpr (P == 5) {
@@ -433,10 +463,14 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
       const bool load = need && !exhausted;
       if (load) cp_async_wait_all();  // this lane's copies of `spot` have landed
       group_sync<SLOTS>();             // ... and every other lane's
+      const PX* win = reinterpret_cast<const PX*>(S.stage + gib * S.sw) + nsh;
+      // G = sum g (model.py:223); it is non-finite iff some pixel is (a sum of <= 1024 finite
+      // f32 values cannot overflow f64), so it doubles as the InvalidInput pixel check
+      bool sgt, sg40, sint = true;
+      const double gsum = load_spot<P, SLOTS, FULL, PX>(S, win, load, L.own, L.base, L.tbase, L.ch, L.tl, sgt, sg40,
+                                                        fused ? &sint : nullptr);
       bool bad = false;
-      if (fused)
-        fused_init<P, SLOTS, PX>(reinterpret_cast<const PX*>(S.stage + gib * S.sw) + nsh, load, geom, cfg,
-                                 L.lg.invW, L.gl, nxt);
+      if (fused) fused_init<P, SLOTS, PX>(win, load, group_all<SLOTS>(sint), geom, cfg, L.lg.invW, L.gl, nxt);
       if (load) {
         float init[P];
         double v[P];
@@ -455,12 +489,6 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
 #pragma unroll
         for (int k = 0; k < P; ++k) s.best[k] = init[k];
       }
-      // G = sum g (model.py:223); it is non-finite iff some pixel is (a sum of <= 1024 finite
-      // f32 values cannot overflow f64), so it doubles as the InvalidInput pixel check
-      bool sgt, sg40;
-      const double gsum =
-          load_spot<P, SLOTS, FULL, PX>(S, reinterpret_cast<const PX*>(S.stage + gib * S.sw) + nsh, load, L.own,
-                                        L.base, L.tbase, L.ch, L.tl, sgt, sg40);
       group_sync<SLOTS>();  // the staging window has been read: refill it
       const int64_t nxt_spot = claim(load);
       if (load) {

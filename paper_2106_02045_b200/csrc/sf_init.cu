@@ -12,93 +12,157 @@ namespace sf {
 
 namespace {
 
-// Standalone initializer: one warp per spot, persistent over spots.  Each spot is
-// widened once into a zero-padded (W+2) x (H+2) f64 tile in shared memory, so the
-// 3x3 window needs no bounds checks and no per-tap conversion: the padding adds
-// +0.0, which leaves every partial sum unchanged (a sum that starts at +0.0 is
-// never -0.0), so the row-major f64 sum is sf_init_core.cuh's bit for bit.  The
-// in-bounds count is (1 + [x>0] + [x<W-1]) (1 + [y>0] + [y<H-1]).
+// Standalone initializer.  A warp takes G = 32 / L spots at a time (L lanes per
+// spot: the smallest of 8, 16, 32 that covers a row, so every lane walks a
+// column), persistent over the batch.  The next G spots stream into the warp's
+// second staging buffer with cp.async while the current ones are scanned (one
+// coalesced window per G spots: 16-byte copies, element copies only where the
+// window pokes out of the caller's array), so the HBM latency is hidden and the
+// per-spot reductions are shared by G spots per instruction.  A tame spot (every
+// pixel an integer in [0, 2^20]: camera counts) takes the exact integer column
+// walk of sf_init_core.cuh; any other spot the general f64 scan.
 constexpr int kInitWarps = 8;
-__global__ void __launch_bounds__(32 * kInitWarps) init_kernel(const float* __restrict__ images, int W, int H,
+
+template <typename PX>
+__host__ __device__ constexpr int init_buf_elems(int G, int N) {
+  // the 16-B aligned window around G*N pixels, in PX units (+ one 16-B line of slack each side)
+  return ((G * N * (int)sizeof(PX) + 47) & ~15) / (int)sizeof(PX);
+}
+
+template <int L, typename PX>
+__global__ void __launch_bounds__(32 * kInitWarps) init_kernel(const PX* __restrict__ images, int W, int H,
                                                               int64_t count, int P, double smin, double smax,
                                                               float* __restrict__ inits, float* __restrict__ amps) {
-  extern __shared__ double init_tile[];  // [kInitWarps][(W + 2) * (H + 2)]
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const int N = W * H, PW = W + 2, PN = (W + 2) * (H + 2);
-  double* t = init_tile + warp * PN;
-  for (int i = lane; i < PN; i += 32) t[i] = 0.0;  // borders stay +0.0; the interior is rewritten per spot
+  constexpr int G = 32 / L;
+  extern __shared__ __align__(16) unsigned char init_smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sub = lane / L, sl = lane % L;  // spot of the warp's G, lane within the spot
+  const int N = W * H;
+  const int be = init_buf_elems<PX>(G, N);
+  PX* buf = reinterpret_cast<PX*>(init_smem) + (size_t)warp * 2 * be;
   const float invW = 1.0f / (float)W;
+  const int64_t ntask = (count + G - 1) / G;
   const int64_t stride = (int64_t)gridDim.x * kInitWarps;
+  const uintptr_t lo = (uintptr_t)images, hi = (uintptr_t)(images + count * (int64_t)N);
+  // stage task t (spots t*G .. t*G+G-1) into buffer b; returns the first spot's element offset
+  auto stage = [&](int64_t t, int b) -> int {
+    const PX* src = images + t * G * (int64_t)N;
+    const uintptr_t a0 = (uintptr_t)src & ~(uintptr_t)15;
+    uintptr_t e0 = ((uintptr_t)(src + G * (int64_t)N) + 15) & ~(uintptr_t)15;
+    if (e0 > ((hi + 15) & ~(uintptr_t)15)) e0 = (hi + 15) & ~(uintptr_t)15;
+    const int nck = (int)((e0 - a0) >> 4);
+    PX* dst = buf + b * be;
+    for (int c = lane; c < nck; c += 32) {
+      const uintptr_t cs = a0 + 16 * (uintptr_t)c;
+      float* d = reinterpret_cast<float*>(dst) + 4 * c;
+      if (cs >= lo && cs + 16 <= hi) {
+        cp_async16(d, reinterpret_cast<const void*>(cs));
+      } else {  // the window pokes out of the caller's array: in-bounds elements only
+#pragma unroll
+        for (int w = 0; w < 16 / (int)sizeof(PX); ++w)
+          if (cs + sizeof(PX) * w >= lo && cs + sizeof(PX) * (w + 1) <= hi)
+            reinterpret_cast<PX*>(d)[w] = *reinterpret_cast<const PX*>(cs + sizeof(PX) * w);
+      }
+    }
+    return (int)(((uintptr_t)src & 15) / sizeof(PX));
+  };
+  int64_t t = (int64_t)blockIdx.x * kInitWarps + warp;
+  int off[2] = {0, 0};
+  if (t < ntask) off[0] = stage(t, 0);
+  cp_async_commit();
 #pragma unroll 1
-  for (int64_t spot = (int64_t)blockIdx.x * kInitWarps + warp; spot < count; spot += stride) {
-    const float* g = images + spot * (int64_t)N;
-    __syncwarp();  // the previous spot's tile reads are done
-#pragma unroll 4
-    for (int i = lane; i < N; i += 32) {
-      const int y = (int)(((float)i + 0.5f) * invW);
-      t[(y + 1) * PW + (i - y * W) + 1] = (double)__ldcs(g + i);
-    }
+  for (int i = 0; t < ntask; t += stride, ++i) {
+    const int b = i & 1;
+    if (t + stride < ntask) off[b ^ 1] = stage(t + stride, b ^ 1);
+    cp_async_commit();
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // this task's copies have landed
     __syncwarp();
-    InitPart p;
-    init_part_reset(p);
-#pragma unroll 2
-    for (int i = lane; i < N; i += 32) {
-      const int y = (int)(((float)i + 0.5f) * invW);
-      const int x = i - y * W;
-      const double* c = t + y * PW + x;  // top-left of the padded window
-      double s = 0.0;
-#pragma unroll
-      for (int dy = 0; dy < 3; ++dy)
-#pragma unroll
-        for (int dx = 0; dx < 3; ++dx) s = __dadd_rn(s, c[dy * PW + dx]);
-      const int cnt = (1 + (x > 0) + (x < W - 1)) * (1 + (y > 0) + (y < H - 1));
-      const float v = (float)(s / (double)cnt);
-      if (v != v) p.nan |= i == 0 ? 3 : 1;
-      init_part_merge(p, v, i, v, 0);
+    const int64_t spot = t * G + sub;
+    const bool valid = spot < count;
+    const PX* sp = buf + b * be + off[b] + sub * N;
+    bool tame = true;
+    if (valid) {
+      for (int j = sl; j < N; j += L) {
+        const float v = (float)sp[j];
+        tame = tame && __float_as_uint(v) <= 0x49800000u && __fsub_rn(__fadd_rn(v, 8388608.0f), 8388608.0f) == v;
+      }
     }
+    int tm = tame ? 1 : 0;  // AND over the spot's lanes (every lane shuffles: no short-circuit)
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-      init_part_merge(p, __shfl_xor_sync(kFull, p.best, o), __shfl_xor_sync(kFull, p.idx, o),
-                      __shfl_xor_sync(kFull, p.lo, o), __shfl_xor_sync(kFull, p.nan, o));
+    for (int o = 1; o < L; o <<= 1) tm &= __shfl_xor_sync(kFull, tm, o);
+    tame = tm != 0;
+    InitScan a;
+    scan_reset(a);
+    if (valid) {
+      if (tame)
+        init_scan_tame<L, PX>(sp, W, H, sl, a);
+      else
+        init_scan(sp, W, H, N, invW, sl, L, a);
+    }
+    scan_reduce<L>(a);
     int idx;
     float alpha, beta;
     double thr;
-    init_finish(p, idx, alpha, beta, thr);
+    init_finish(a, idx, alpha, beta, thr);
     int m = 0;
-    for (int i = lane; i < N; i += 32) {
-      const int y = (int)(((float)i + 0.5f) * invW);
-      m += (t[(y + 1) * PW + (i - y * W) + 1] > thr) ? 1 : 0;
-    }
+    if (valid) m = tame ? init_count_tame(sp, N, thr, sl, L) : init_count(sp, N, thr, sl, L);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m += __shfl_xor_sync(kFull, m, o);
-    const float sg = init_sigma(m, smin, smax);
-    if (lane < P) {
-      const float v = lane == 0 ? (float)(idx % W) : (lane == 1 ? (float)(idx / W) : sg);
-      inits[spot * P + lane] = v;
+    for (int o = 1; o < L; o <<= 1) m += __shfl_xor_sync(kFull, m, o);
+    if (valid) {
+      const float sg = init_sigma(m, smin, smax);
+      if (sl < P) {  // (x, y, sigma[, sigma]); P = 5 (explicit-5, internal): (x, y, sigma, alpha, beta)
+        const int y = (int)(((float)idx + 0.5f) * invW);  // idx / W exactly (see init_smoothed)
+        inits[spot * P + sl] = sl == 0 ? (float)(idx - y * W)
+                                       : (sl == 1 ? (float)y : (sl == 2 || P == 4 ? sg : (sl == 3 ? alpha : beta)));
+      }
+      if (amps != nullptr && sl < 2) amps[2 * spot + sl] = sl == 0 ? alpha : beta;
     }
-    if (amps != nullptr && lane < 2) amps[2 * spot + lane] = lane == 0 ? alpha : beta;
+    __syncwarp();  // buffer b is restaged two tasks later
   }
+  cp_async_wait_all();
 }
-}  // namespace
 
-cudaError_t launch_estimate_initial(const float* images, int W, int H, int64_t count, int P, double sigma_min,
-                                    double sigma_max, float* inits, float* amps, cudaStream_t stream) {
-  if (count <= 0) return cudaSuccess;
-  const size_t smem = (size_t)kInitWarps * (W + 2) * (H + 2) * sizeof(double);  // <= 66 KB (N <= 1024)
-  cudaError_t e = cudaFuncSetAttribute(init_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+template <int L, typename PX>
+cudaError_t launch_init_l(const PX* images, int W, int H, int64_t count, int P, double smin, double smax,
+                          float* inits, float* amps, cudaStream_t stream) {
+  constexpr int G = 32 / L;
+  const size_t smem = (size_t)kInitWarps * 2 * init_buf_elems<PX>(G, W * H) * sizeof(PX);  // <= 66 KB
+  auto kern = init_kernel<L, PX>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, per_sm = 0;
   if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
   if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, init_kernel, 32 * kInitWarps, smem)) != cudaSuccess)
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * kInitWarps, smem)) != cudaSuccess)
     return e;
   int64_t blocks = (int64_t)(per_sm > 0 ? per_sm : 1) * sms;
-  const int64_t need = (count + kInitWarps - 1) / kInitWarps;
+  const int64_t need = ((count + G - 1) / G + kInitWarps - 1) / kInitWarps;
   if (blocks > need) blocks = need;
-  init_kernel<<<(unsigned)blocks, 32 * kInitWarps, smem, stream>>>(images, W, H, count, P, sigma_min, sigma_max,
-                                                                   inits, amps);
+  kern<<<(unsigned)blocks, 32 * kInitWarps, smem, stream>>>(images, W, H, count, P, smin, smax, inits, amps);
   return cudaGetLastError();
+}
+}  // namespace
+
+template <typename PX>
+cudaError_t launch_init_px(const PX* images, int W, int H, int64_t count, int P, double sigma_min, double sigma_max,
+                           float* inits, float* amps, cudaStream_t stream) {
+  if (count <= 0) return cudaSuccess;
+  // L lanes per spot: enough to give every lane a column, and G * N <= 1024 pixels per warp buffer
+  const int N = W * H;
+  if (W > 16 || N > 512) return launch_init_l<32, PX>(images, W, H, count, P, sigma_min, sigma_max, inits, amps, stream);
+  if (W > 8 || N > 256) return launch_init_l<16, PX>(images, W, H, count, P, sigma_min, sigma_max, inits, amps, stream);
+  return launch_init_l<8, PX>(images, W, H, count, P, sigma_min, sigma_max, inits, amps, stream);
+}
+
+cudaError_t launch_estimate_initial(const float* images, int W, int H, int64_t count, int P, double sigma_min,
+                                    double sigma_max, float* inits, float* amps, cudaStream_t stream) {
+  return launch_init_px<float>(images, W, H, count, P, sigma_min, sigma_max, inits, amps, stream);
+}
+
+cudaError_t launch_estimate_initial_u16(const uint16_t* images, int W, int H, int64_t count, int P,
+                                        double sigma_min, double sigma_max, float* inits, float* amps,
+                                        cudaStream_t stream) {
+  return launch_init_px<uint16_t>(images, W, H, count, P, sigma_min, sigma_max, inits, amps, stream);
 }
 
 // Exhaustive-check helper: numpy exp on the device (variant 0: production
@@ -134,6 +198,24 @@ __global__ void ddiv_kernel(const double* __restrict__ a, const double* __restri
     out[i] = (__double_as_longlong(w) == __double_as_longlong(f) || (w != w && f != f)) ? w
                                                                                     : __longlong_as_double(0x7ff8dead0000beefull);
   }
+}
+
+// Exhaustive check of the initializer's integer-path division: tame_div(s, c) == __fdiv_rn(s, c)
+// for every integer s in [0, 9 * 2^20] and c in {1, 2, 3, 4, 6, 9}; counts mismatches.
+__global__ void tame_div_kernel(unsigned long long* mismatches) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n = 9LL * 1048576 + 1;
+  if (t >= 6 * n) return;
+  const int cs[6] = {1, 2, 3, 4, 6, 9};
+  const float c = (float)cs[t / n];
+  const float s = (float)(t % n);
+  if (__float_as_uint(tame_div(s, c, __frcp_rn(c))) != __float_as_uint(__fdiv_rn(s, c))) atomicAdd(mismatches, 1ull);
+}
+
+cudaError_t launch_tame_div(unsigned long long* mismatches, cudaStream_t stream) {
+  const int64_t n = 6 * (9LL * 1048576 + 1);
+  tame_div_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(mismatches);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_ddiv(const double* a, const double* b, double* out, int64_t n, cudaStream_t stream) {

@@ -51,9 +51,33 @@ int launch_fit_P5_S4(const LaunchFit& a, cudaError_t* err);
 int launch_fit_P5_S8(const LaunchFit& a, cudaError_t* err);
 int launch_fit_P5_S16(const LaunchFit& a, cudaError_t* err);
 
-// initializer kernel launcher (sf_init.cu)
+// initializer kernel launchers (sf_init.cu): float pixels, 16-bit counts
 cudaError_t launch_estimate_initial(const float* images, int W, int H, int64_t count, int P, double sigma_min,
                                     double sigma_max, float* inits, float* amps, cudaStream_t stream);
+cudaError_t launch_estimate_initial_u16(const uint16_t* images, int W, int H, int64_t count, int P,
+                                        double sigma_min, double sigma_max, float* inits, float* amps,
+                                        cudaStream_t stream);
+// Batches up to this many spots with inits == NULL use the fit kernel's fused initializer (one
+// kernel, the latency path); larger ones run the standalone initializer in front of the fit on the
+// same stream, which keeps the fit kernel's instruction working set small (the fused path costs
+// ~20% of fit time at 15x15 in i-cache misses: profiles/r02_fused_init.txt).
+constexpr int64_t kFusedInitMaxSpots = 16384;
+
+// spotfit.model function surface (sf_model.cu)
+cudaError_t launch_model_profile(const float* params, int W, int H, int64_t count, int P, float* f, float* fgrad,
+                                 cudaStream_t st);
+cudaError_t launch_model_alpha_beta(const float* f, const float* g, int N, int64_t count, float* alpha, float* beta,
+                                    double* sums, int32_t* singular, cudaStream_t st);
+cudaError_t launch_model_chi(const float* g, const float* f, const float* alpha, const float* beta, int N,
+                             int64_t count, float* h, float* r, float* chi, cudaStream_t st);
+cudaError_t launch_model_gradient_sums(const float* f, const float* fgrad, const float* g, const double* sums, int N,
+                                       int P, int64_t count, double* out, cudaStream_t st);
+cudaError_t launch_model_coefficient_gradients(const double* sums, const double* gsums, const float* alpha,
+                                               const float* beta, int N, int P, int64_t count, double* dalpha,
+                                               double* dbeta, int32_t* singular, cudaStream_t st);
+cudaError_t launch_model_chi_gradient(const float* g, const float* f, const float* fgrad, const float* alpha,
+                                      const float* beta, const double* dalpha, const double* dbeta, int N, int P,
+                                      int64_t count, double* grad, float* dmat, cudaStream_t st);
 
 // device simulator (sf_sim.cu)
 cudaError_t launch_simulate(const sf_sim_config& c, int W, int H, int64_t first, int64_t count, float* images,
@@ -62,6 +86,9 @@ cudaError_t launch_simulate(const sf_sim_config& c, int W, int H, int64_t first,
 
 // shared-divisor f64 division check (sf_init.cu)
 cudaError_t launch_ddiv(const double* a, const double* b, double* out, int64_t n, cudaStream_t stream);
+
+// initializer integer-path division check (sf_init.cu)
+cudaError_t launch_tame_div(unsigned long long* mismatches, cudaStream_t stream);
 
 // exhaustive-check helper (sf_init.cu)
 cudaError_t launch_npexp(const float* x, float* y, int64_t n, int variant, cudaStream_t stream);

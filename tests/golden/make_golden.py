@@ -169,8 +169,68 @@ def pwsum_golden():
     np.savez_compressed(os.path.join(HERE, "pwsum_golden.npz"), x=np.array(xs), s=np.array(sums), n=np.array(ns))
 
 
+def model_pixels_golden():
+    """Per-pixel outputs of every spotfit.model function (h, r, dmat besides f, fgrad), also on
+    profile / gradient arrays that did not come from profile_and_gradient (uniform random f in
+    [0, 1), normal fgrad): the GPU's sf_model_* entry points are checked against these."""
+    rng = np.random.default_rng(20260101)
+    rec = {k: [] for k in ("shape", "image", "params", "f", "fgrad", "f_profile", "kind", "singular", "alpha", "beta",
+                           "sums", "h", "r", "chi", "gsums", "dalpha", "dbeta", "grad", "dmat")}
+    for (W, H) in SHAPES:
+        N = W * H
+        im, tr = simulate_batch(SimConfig(width=W, height=H, count=4, seed=5000 + N))
+        for s in range(4):
+            g = im[s].reshape(-1).astype(np.float32)
+            x, y, sg = tr[s][:3]
+            sp = ref.ShapeParams(x + rng.normal(0, 0.3), y + rng.normal(0, 0.3), sg * rng.uniform(0.7, 1.4))
+            grid = ref.PixelGrid(W, H)
+            img = ref.SpotImage(grid, g)
+            f_prof = ref.profile(sp, grid)
+            if s < 2:  # the reference chain as the solver runs it
+                f, fg = ref.profile_and_gradient(sp, grid)
+                kind = 0
+            else:  # arbitrary arrays through the same functions
+                f = rng.uniform(0.0, 1.0, N).astype(np.float32)
+                fg = rng.normal(0.0, 1.0, (N, 3)).astype(np.float32)
+                kind = 1
+            if s == 3:
+                f = np.full(N, 0.25, np.float32)  # constant profile: SingularProfile
+            row = dict(shape=(W, H), image=np.pad(g, (0, 1024 - N)),
+                       params=np.array([sp.x, sp.y, sp.sigma], np.float32), f=np.pad(f, (0, 1024 - N)),
+                       fgrad=np.pad(fg, ((0, 1024 - N), (0, 0))), f_profile=np.pad(f_prof, (0, 1024 - N)), kind=kind)
+            try:
+                amps, sums = ref.alpha_beta(f, img)
+                h = ref.model_values(f, amps)
+                r = ref.residuals(img, f, amps)
+                chi = ref.chi_squared(img, f, amps)
+                gs = ref.gradient_sums(f, fg, img, sums)
+                cg = ref.coefficient_gradients(sums, gs, amps)
+                grad, d = ref.chi_gradient(img, f, fg, amps, cg)
+                row.update(singular=0, alpha=amps.alpha, beta=amps.beta,
+                           sums=[sums.f_sum, sums.g_sum, sums.ff_sum, sums.fg_sum, sums.denom],
+                           h=np.pad(h, (0, 1024 - N)), r=np.pad(r, (0, 1024 - N)), chi=chi,
+                           gsums=np.stack([gs.df, gs.dff, gs.dfg, gs.gamma]), dalpha=cg[0], dbeta=cg[1], grad=grad,
+                           dmat=np.pad(d, ((0, 1024 - N), (0, 0))))
+            except ref.SingularProfile:
+                nan = np.float32(np.nan)
+                row.update(singular=1, alpha=nan, beta=nan, sums=[np.nan] * 5, h=np.zeros(1024, np.float32),
+                           r=np.zeros(1024, np.float32), chi=nan, gsums=np.zeros((4, 3)), dalpha=np.zeros(3),
+                           dbeta=np.zeros(3), grad=np.zeros(3), dmat=np.zeros((1024, 3), np.float32))
+            for k, v in row.items():
+                rec[k].append(v)
+    out = {}
+    for k, v in rec.items():
+        a = np.array(v)
+        if k in ("alpha", "beta", "chi", "f", "fgrad", "f_profile", "h", "r", "dmat", "image", "params"):
+            a = a.astype(np.float32)
+        out[k] = a
+    np.savez_compressed(os.path.join(HERE, "model_pixels_golden.npz"), **out)
+    print("model_pixels_golden:", len(rec["alpha"]), "cases")
+
+
 if __name__ == "__main__":
-    model_golden()
-    fit_golden()
-    npexp_golden()
-    pwsum_golden()
+    import sys as _sys
+
+    which = _sys.argv[1:] or ["model", "fit", "npexp", "pwsum", "model_pixels"]
+    for name in which:
+        globals()[f"{name}_golden"]()

@@ -68,6 +68,58 @@ def test_fused_init_equals_standalone_initializer(sf, W, H, engine):
     _same(sf.fit_batch(torch.from_numpy(u).cuda(), grid=grid, engine=engine), ref, f"device u16 {W}x{H} {engine}")
 
 
+@pytest.mark.parametrize("W,H,engine", [(15, 15, "implicit3"), (11, 11, "implicit3"), (21, 21, "elliptical"),
+                                        (32, 32, "implicit3"), (13, 11, "explicit5"), (5, 40, "implicit3"),
+                                        (1, 200, "implicit3")])
+def test_inits_none_large_batches(sf, W, H, engine):
+    """Batches above the fused-initializer size (sf_launch.h:kFusedInitMaxSpots) run the standalone
+    initializer in front of the fit -- per host chunk, or into a stream-ordered scratch buffer for
+    device batches -- with the same results as explicit standalone inits; mixed tame / general spots."""
+    import torch
+
+    P = sf.batch_engine.ENGINES[engine]
+    count = 40_001
+    im = _sim(sf, W, H, count, seed=5 + W * H, model=4 if P == 4 else 3).astype(np.float32)
+    im[::7] += np.float32(0.25)  # general (non-integer) spots interleaved with tame ones
+    grid = sf.PixelGrid(W, H)
+    ref = sf.fit_batch(im, _standalone_inits(sf, im, W, H, P), grid=grid, engine=engine)
+    _same(sf.fit_batch(im, grid=grid, engine=engine), ref, f"host f32 {W}x{H} {engine}")
+    _same(sf.fit_batch(torch.from_numpy(im).cuda(), grid=grid, engine=engine), ref, f"device f32 {W}x{H} {engine}")
+    ti = np.round(im[1::7])  # integer spots only for the u16 paths
+    u = ti.astype(np.uint16)
+    ref16 = sf.fit_batch(ti, _standalone_inits(sf, ti, W, H, P), grid=grid, engine=engine)
+    _same(sf.fit_batch(u, grid=grid, engine=engine), ref16, f"host u16 {W}x{H} {engine}")
+    big = np.concatenate([u] * 4)
+    refb = sf.fit_batch(big.astype(np.float32), _standalone_inits(sf, big.astype(np.float32), W, H, P), grid=grid,
+                        engine=engine)
+    _same(sf.fit_batch(torch.from_numpy(big).cuda(), grid=grid, engine=engine), refb, f"device u16 {W}x{H} {engine}")
+
+
+@pytest.mark.parametrize("W,H,engine", [(15, 15, "implicit3"), (32, 32, "implicit3"), (5, 40, "implicit3"),
+                                        (21, 21, "elliptical"), (13, 11, "explicit5")])
+def test_fused_init_integer_and_general_paths(sf, W, H, engine):
+    """The fused initializer's exact integer path (every pixel an integer in [0, 2^20]) and its
+    general f64 path, interleaved spot by spot inside one batch (so groups of one warp take
+    different paths): fractional pixels, integers above 2^20, -0.0, tiny and negative values."""
+    P = sf.batch_engine.ENGINES[engine]
+    count = 4000
+    im = _sim(sf, W, H, count, seed=77 + W, model=4 if P == 4 else 3).astype(np.float32)
+    rng = np.random.default_rng(W * H)
+    k = np.arange(count) % 8
+    im[k == 1] += np.float32(0.5)  # fractional
+    im[k == 2] *= np.float32(4096.0)  # integers above 2^20 (the peak)
+    im[k == 3, 0] = np.float32(-0.0)
+    im[k == 4, rng.integers(0, W * H)] = np.float32(1e-30)
+    im[k == 5] -= np.float32(3.0)  # negative background
+    im[k == 6] = np.float32(1048576.0)  # exactly 2^20: still the integer path
+    grid = sf.PixelGrid(W, H)
+    ref = sf.fit_batch(im, _standalone_inits(sf, im, W, H, P), grid=grid, engine=engine)
+    _same(sf.fit_batch(im, grid=grid, engine=engine), ref, f"mixed paths {W}x{H} {engine}")
+    oi, oa = oinit.estimate_initial_batch_np(im, W, H, 0.3, float(max(W, H)), 3 if P == 5 else P)
+    si, sa = sf.estimate_initial_batch(im, 3 if P == 5 else P, grid=grid)
+    assert bits_equal(si, oi) and bits_equal(sa, oa)
+
+
 def test_fused_init_matches_oracle_end_to_end(sf, oracle_lib):
     """inits=None against the C oracle driven by the oracle initializer (oracle/initializer.py)."""
     W = H = 15
@@ -234,3 +286,14 @@ def test_work_slots_never_shared_under_load(sf, oracle_lib):
         assert bits_equal(b["par"].cpu().numpy(), ref["params"])
         assert bits_equal(b["u8"][0].cpu().numpy(), ref["status"])
         assert bits_equal(b["u8"][1].cpu().numpy(), ref["iterations"])
+
+
+def test_tame_division_exhaustive(sf):
+    """The initializer's integer-path division (sf_init_core.cuh:tame_div: multiply by the
+    rounded reciprocal, one exact-residual correction) equals IEEE s / c for every integer
+    s in [0, 9 * 2^20] and every truncated-window count c in {1, 2, 3, 4, 6, 9}."""
+    import torch
+
+    m = torch.zeros(1, dtype=torch.int64, device="cuda")
+    sf._lib.check(sf._lib.lib().sf_debug_tame_div_device(m.data_ptr(), torch.cuda.current_stream().cuda_stream))
+    assert int(m.item()) == 0

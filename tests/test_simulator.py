@@ -78,6 +78,52 @@ def test_python_restatement_of_the_stream():
         assert np.float32(cx) == tr[idx, 0] and np.float32(sg) == tr[idx, 2]
 
 
+@pytest.mark.parametrize("W,H,model,kw", [(15, 15, 3, {}), (21, 21, 4, {}), (11, 11, 3, {"first_index": 10**9}),
+                                           (32, 32, 3, {"spread": 2.5}), (7, 5, 4, {"noise": False}),
+                                           (9, 9, 3, {"noise": False, "rounding": False}),
+                                           (13, 3, 3, {"n_signal": 4000.0, "n_background": 400.0})])
+def test_numpy_restatement_equals_host_generator(W, H, model, kw):
+    """oracle/simulator.py (vectorised numpy Philox + Box-Muller + SPEC.md:335-358 noise) equals
+    the product's host generator bit for bit on every pixel and truth value."""
+    import paper_2106_02045_b200 as sf
+    from oracle import simulator as osim
+
+    first = kw.pop("first_index", 0)
+    count = 3000
+    a, ta = osim.simulate_batch(W, H, count, seed=0xDEADBEEF12345, model=model, first_index=first, **kw)
+    ckw = {("center_spread" if k == "spread" else k): v for k, v in kw.items()}
+    b, tb = sf.simulate_batch(sf.SimConfig(width=W, height=H, count=count, seed=0xDEADBEEF12345, model=model, **ckw),
+                              first_index=first)
+    assert bits_equal(a, b) and bits_equal(ta, tb)
+
+
+@pytest.mark.gpu
+def test_device_simulator_matches_independent_restatement():
+    """Every pixel of sampled spots of the DEVICE generator against the independent numpy
+    restatement (oracle/simulator.py): equal except where the unrounded value lies within
+    1e-6 of a .5 rounding boundary (CUDA's f64 libm and numpy's may differ in the last ulp)."""
+    import torch
+
+    import paper_2106_02045_b200 as sf
+    from oracle import simulator as osim
+
+    for model, W, count in ((3, 15, 200_000), (4, 21, 50_000), (3, 32, 20_000)):
+        cfg = sf.SimConfig(width=W, height=W, count=count, seed=2021, model=model)
+        di, dt = sf.simulate_batch_device(cfg)
+        torch.cuda.synchronize()
+        idx = np.unique(np.linspace(0, count - 1, 1500).astype(np.int64))
+        di, dt = di.cpu().numpy()[idx].reshape(len(idx), -1), dt.cpu().numpy()[idx]
+        oi = np.concatenate([osim.simulate_batch(W, W, 1, 2021, model, first_index=int(i))[0].reshape(1, -1)
+                             for i in idx])
+        ot = np.concatenate([osim.simulate_batch(W, W, 1, 2021, model, first_index=int(i))[1] for i in idx])
+        rows, cols = np.nonzero(di != oi)
+        for r, c in zip(rows, cols):
+            v = osim.unrounded(W, W, int(idx[r]), 2021, model)[c]
+            assert abs(abs(v - np.trunc(v)) - 0.5) < 1e-6 and abs(di[r, c] - oi[r, c]) == 1, (model, idx[r], c, v)
+        rel = np.abs(dt.astype(np.float64) - ot) / np.maximum(np.abs(ot), 1e-30)
+        assert rel.max() < 1e-6 and (dt == ot).mean() > 0.999
+
+
 @pytest.mark.gpu
 def test_device_simulator_matches_host():
     import torch
