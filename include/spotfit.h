@@ -260,6 +260,38 @@ int sf_debug_ddiv_device(const double* d_a, const double* d_b, double* d_out, in
  */
 int sf_debug_tame_div_device(uint64_t* d_mismatches, void* stream);
 
+/*
+ * ParamsCSV / truth CSV (cmd_fit writes, cmd_assess reads, SPEC.md:536-549;
+ * round trip SPEC.md:554).  Host-only, multi-threaded (threads <= 0: all hardware threads).
+ * The reference CLI is SPEC-only (no code under /root/reference); its Python restatement in
+ * paper_2106_02045_b200/io_formats.py (fmt32: numpy's format_float_positional(unique=True,
+ * trim='-')) is the checker.  Floats are rendered as the shortest decimal that round-trips the
+ * float32 value, positional notation.  Every row is `index,<cells>` with index = first_index + r.
+ */
+enum sf_csv_kind {
+  SF_CSV_F32 = 0,   /* float32, shortest round-trip positional */
+  SF_CSV_U8 = 1,    /* uint8 as a decimal integer (iterations) */
+  SF_CSV_STOP = 2,  /* status byte & 7 as the StopReason name (MaxError .. MaxIterations) */
+  SF_CSV_FLAGS = 3, /* status byte & 0xf8 as a decimal integer (0x40 invalid, 0x80 no-improvement) */
+  SF_CSV_SKIP = 4   /* reader only: ignore the column */
+};
+typedef struct sf_csv_col {
+  int32_t kind;   /* sf_csv_kind */
+  void* data;     /* element r of the column is data[r * stride] */
+  int64_t stride; /* in elements */
+} sf_csv_col;
+
+/* write `header` + '\n' then `rows` rows; returns 0 or -1 (message: sf_csv_last_error()) */
+int sf_csv_write(const char* path, const char* header, int64_t first_index, int64_t rows, int ncols,
+                 const sf_csv_col* cols, int threads);
+/* parse the rows after the header line: *rows_out = row count; capacity < 0 counts only; index may be
+ * NULL; a row whose cells do not match `cols` exactly fails with its row number */
+int sf_csv_read(const char* path, int64_t* rows_out, int64_t* index, int ncols, const sf_csv_col* cols,
+                int64_t capacity, int threads);
+/* diagnostic: the float32 rendering alone, one value per line into out (capacity bytes) */
+int sf_format_f32(const float* values, int64_t count, char* out, int64_t capacity, int64_t* out_len);
+const char* sf_csv_last_error(void);
+
 int sf_device_count(void);
 const char* sf_last_error(void);
 int sf_version(void);

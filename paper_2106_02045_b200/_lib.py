@@ -91,6 +91,12 @@ class sf_sim_config(ctypes.Structure):
     ]
 
 
+class sf_csv_col(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("data", ctypes.c_void_p), ("stride", ctypes.c_int64)]
+
+
+SF_CSV_F32, SF_CSV_U8, SF_CSV_STOP, SF_CSV_FLAGS, SF_CSV_SKIP = range(5)
+
 # symbol -> (restype, argtypes); the exact set include/spotfit.h declares
 _vp, _i32, _i64, _f64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
 SYMBOLS = {
@@ -118,6 +124,12 @@ SYMBOLS = {
     "sf_debug_npexp_device": (ctypes.c_int, [_vp, _vp, _i64, _i32, _vp]),
     "sf_debug_ddiv_device": (ctypes.c_int, [_vp, _vp, _vp, _i64, _vp]),
     "sf_debug_tame_div_device": (ctypes.c_int, [_vp, _vp]),
+    "sf_csv_write": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p, _i64, _i64, ctypes.c_int,
+                                    ctypes.POINTER(sf_csv_col), ctypes.c_int]),
+    "sf_csv_read": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int64), _vp, ctypes.c_int,
+                                   ctypes.POINTER(sf_csv_col), _i64, ctypes.c_int]),
+    "sf_format_f32": (ctypes.c_int, [_vp, _i64, _vp, _i64, ctypes.POINTER(ctypes.c_int64)]),
+    "sf_csv_last_error": (ctypes.c_char_p, []),
     "sf_host_alloc": (ctypes.c_void_p, [ctypes.c_size_t]),
     "sf_host_free": (None, [_vp]),
     "sf_device_count": (ctypes.c_int, []),

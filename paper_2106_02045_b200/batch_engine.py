@@ -175,7 +175,7 @@ def fit_batch(images, inits=None, config: FitConfig = FitConfig(), engine: str =
         out = BatchResult(np.empty((count, P), np.float32), np.empty(count, np.float32), np.empty(count, np.float32),
                           np.empty(count, np.float32), np.empty(count, np.uint8), np.empty(count, np.uint8))
     st = _lib.sf_stats()
-    devs = list(devices) if devices else [0]
+    devs = [_device_index(d) for d in devices] if devices else [0]
     dev_arr = (ctypes.c_int32 * len(devs))(*devs)
     entry = L.sf_fit_batch_u16 if imgs.dtype == np.uint16 else L.sf_fit_batch
     _lib.check(entry(_ptr(imgs), grid.width, grid.height, count, None if ini is None else _ptr(ini),
@@ -185,6 +185,23 @@ def fit_batch(images, inits=None, config: FitConfig = FitConfig(), engine: str =
                      n_kernel_evals=st.n_kernel_evals, total_ms=st.total_ms, n_devices=st.n_devices,
                      n_chunks=st.n_chunks)
     return out
+
+
+def _device_index(d) -> int:
+    """A device given as an int, "cuda:N" / "N" or a torch.device -> its CUDA ordinal."""
+    if isinstance(d, int):
+        return d
+    if type(d).__name__ == "device":  # torch.device
+        return int(d.index or 0)
+    s = str(d)
+    if s == "cuda":
+        return 0
+    if s.startswith("cuda:"):
+        s = s[5:]
+    try:
+        return int(s)
+    except ValueError:
+        raise ValueError(f"not a CUDA device: {d!r}") from None
 
 
 def estimate_initial_device(images_cuda, grid: PixelGrid, P: int, config: FitConfig = FitConfig(), amps=False):
