@@ -380,8 +380,10 @@ struct LaneSetup {
 };
 
 // PX: pixel type of `images` -- float, or uint16_t camera counts (sf_fit_batch_u16), staged as
-// u16 and widened exactly in load_spot, so the host pipeline needs no separate widening kernel
-template <int P, int SLOTS, bool FULL, typename PX = float>
+// u16 and widened exactly in load_spot, so the host pipeline needs no separate widening kernel.
+// FUSED: inits == NULL, the refill estimates them (fused_init); a separate instantiation, so the
+// kernel that is given inits carries none of the initializer's code or registers.
+template <int P, int SLOTS, bool FULL, typename PX = float, bool FUSED = false>
 __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
                                   P == 5 ? (SLOTS >= 8 ? 1 : SF_MINB_P5)
                                          : (SLOTS == 8 ? 2 * SF_MINB_P3 : (SLOTS == 16 ? SF_MINB_P3
@@ -415,14 +417,14 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
   // refill waits for the copies, scatters the window into the lanes' pixel
   // slots (load_spot), then starts the following spot's copy.
   float nxt[P];
-  const bool fused = inits == nullptr;  // fused initializer: inits estimated from the staged spot
+  constexpr bool fused = FUSED;  // fused initializer: inits estimated from the staged spot
   int nsh = 0;  // float offset of the staged spot inside its window
   const int gib = L.gib();
   const uintptr_t lo = (uintptr_t)images, hi = (uintptr_t)(images + count * (int64_t)N);
   auto prefetch = [&](int64_t sp) {
     if (sp < count) {
       nsh = stage_spot<P, SLOTS, PX>(S, gib, L.gl, images + sp * (int64_t)N, lo, hi, N);
-      if (!fused) {
+      if constexpr (!fused) {
 #pragma unroll
         for (int k = 0; k < P; ++k) nxt[k] = __ldg(inits + sp * P + k);
       }
@@ -470,7 +472,7 @@ __global__ void __launch_bounds__(threads_per_block<SLOTS>(),
       const double gsum = load_spot<P, SLOTS, FULL, PX>(S, win, load, L.own, L.base, L.tbase, L.ch, L.tl, sgt, sg40,
                                                         fused ? &sint : nullptr);
       bool bad = false;
-      if (fused) fused_init<P, SLOTS, PX>(win, load, group_all<SLOTS>(sint), geom, cfg, L.lg.invW, L.gl, nxt);
+      if constexpr (fused) fused_init<P, SLOTS, PX>(win, load, group_all<SLOTS>(sint), geom, cfg, L.lg.invW, L.gl, nxt);
       if (load) {
         float init[P];
         double v[P];

@@ -15,7 +15,9 @@ namespace sf {
 
 template <typename PX>
 static int launch_fit_px(const LaunchFit& a, const PX* images, cudaError_t* err) {
-  auto kern = a.geom.full ? fit_kernel<SF_P, SF_SLOTS, true, PX> : fit_kernel<SF_P, SF_SLOTS, false, PX>;
+  const bool fused = a.inits == nullptr;
+  auto kern = a.geom.full ? (fused ? fit_kernel<SF_P, SF_SLOTS, true, PX, true> : fit_kernel<SF_P, SF_SLOTS, true, PX, false>)
+                          : (fused ? fit_kernel<SF_P, SF_SLOTS, false, PX, true> : fit_kernel<SF_P, SF_SLOTS, false, PX, false>);
   constexpr int tpb = threads_per_block<SF_SLOTS>();
   constexpr int groups_per_block = SF_SLOTS >= 8 ? 1 : (tpb / 32) * (32 / (8 * SF_SLOTS));
   const size_t smem = Smem<SF_P, SF_SLOTS>::bytes(a.geom.ch, a.geom.tl, a.geom.N);
