@@ -14,6 +14,14 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.fixture(scope="module")
+def sf():
+    import paper_2106_02045_b200 as sf
+
+    sf._lib.require_gpu()
+    return sf
+
+
+@pytest.fixture(scope="module")
 def runs(sf):
     import acceptance as acc
 
