@@ -292,6 +292,13 @@ int sf_csv_read(const char* path, int64_t* rows_out, int64_t* index, int ncols, 
 int sf_format_f32(const float* values, int64_t count, char* out, int64_t capacity, int64_t* out_len);
 const char* sf_csv_last_error(void);
 
+/*
+ * sf_shard_range -- the contiguous spot range [*lo, *hi) of shard `shard` of `n_shards` (the split
+ * sf_fit_batch applies over its devices and a torchrun rank applies over the job): independent,
+ * order-preserving shards, sizes differing by at most one.  Host-only.
+ */
+int sf_shard_range(int64_t count, int32_t shard, int32_t n_shards, int64_t* lo, int64_t* hi);
+
 int sf_device_count(void);
 const char* sf_last_error(void);
 int sf_version(void);

@@ -578,6 +578,14 @@ int sf_lane_geometry(int32_t width, int32_t height, int32_t* slots, int32_t* ppl
   return 0;
 }
 
+int sf_shard_range(int64_t count, int32_t shard, int32_t n_shards, int64_t* lo, int64_t* hi) {
+  if (count < 0 || n_shards < 1 || shard < 0 || shard >= n_shards || !lo || !hi) return fail("bad shard arguments");
+  // contiguous, order-preserving, sizes differ by at most one; exact in 128-bit
+  *lo = (int64_t)((__int128)count * shard / n_shards);
+  *hi = (int64_t)((__int128)count * (shard + 1) / n_shards);
+  return 0;
+}
+
 const char* sf_last_error(void) { return g_err.c_str(); }
 
 int sf_device_count(void) {
@@ -897,8 +905,7 @@ static int fit_batch_impl(const float* images, const uint16_t* images16, int32_t
     j.W = width;
     j.H = height;
     j.P = cfg->model;
-    j.lo = count * d / nd;
-    j.hi = count * (d + 1) / nd;
+    sf_shard_range(count, d, nd, &j.lo, &j.hi);
     j.cfg = cfg;
     j.par = out_params;
     j.alpha = out_alpha;
