@@ -120,7 +120,7 @@ def cmd_fit(a):
     res = fit_batch(flat, inits, config=cfg, engine=a.engine, grid=grid, devices=devices)
     t2 = time.perf_counter()
     try:
-        write_params_csv(a.out, res)
+        write_params_csv(a.out, res, flags=a.flags)
     except OSError as e:
         raise CliError(EXIT_IO, str(e))
     fit_s = t2 - t1
@@ -141,7 +141,13 @@ def cmd_assess(a):
     if len(truth) != len(fits["alpha"]):
         raise CliError(EXIT_ARGS, "fits and truth differ in length")
     stats = accuracy(fits["params"], fits["stop"], truth)
-    report = {"accuracy": stats.as_dict(), "iterations": iteration_stats(fits["stop"], fits["iterations"])}
+    status = fits["stop"] | fits["flags"] if "flags" in fits else fits["stop"]
+    its = iteration_stats(status, fits["iterations"], max(int(a.max_iter), int(fits["iterations"].max(initial=0))))
+    if "flags" not in fits:  # the SPEC header carries the StopReason name only
+        its["no_improvement"] = None
+        its["invalid_input"] = None
+        sys.stderr.write("spotfit assess: no flags column (fit --flags): no-improvement / invalid counts unavailable\n")
+    report = {"accuracy": stats.as_dict(), "iterations": its}
     if a.signal:
         report["expected_error_ratio"] = expected_error_ratio(stats, a.signal)
     _dump(report, a.report)
@@ -211,11 +217,14 @@ def build_parser():
     f.add_argument("--workers", type=int, default=0, help="accepted for compatibility (GPU engine)")
     f.add_argument("--devices", default="")
     f.add_argument("--inits", default="auto")
+    f.add_argument("--flags", action="store_true",
+                   help="append a flags column (status & 0xf8: 64 InvalidInput, 128 no-improvement) for assess")
     a = sub.add_parser("assess")
     a.add_argument("--fits", required=True)
     a.add_argument("--truth", required=True)
     a.add_argument("--report")
     a.add_argument("--signal", type=float, default=0.0)
+    a.add_argument("--max-iter", type=int, default=20, help="histogram range (the fit's --max-iter)")
     b = sub.add_parser("bench")
     b.add_argument("--sizes", default="4,9,16,25,32")
     b.add_argument("--batches", default="10,100,1000,10000")

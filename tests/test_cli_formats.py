@@ -136,3 +136,26 @@ def test_cli_simulate_fit_assess_end_to_end(tmp_path, oracle_lib):
     r = json.load(open(rep))
     assert r["accuracy"]["n_fits"] + r["accuracy"]["n_excluded"] == 1000
     assert 0.02 < r["accuracy"]["position_median"] < 0.1  # Table 1 scale
+
+
+@pytest.mark.gpu
+def test_cli_flags_column_feeds_assess(tmp_path):
+    """fit --flags writes status & 0xf8; assess then counts the no-improvement stops (acceptance
+    criterion 5), which the SPEC header alone cannot carry."""
+    from paper_2106_02045_b200.cli import main
+    from paper_2106_02045_b200.io_formats import read_params_csv
+
+    spb, truth, fits, fits2, rep, rep2 = (tmp_path / n for n in ("s.spb", "t.csv", "f.csv", "g.csv", "r.json",
+                                                               "q.json"))
+    assert main(["simulate", "--size", "9", "--count", "3000", "--seed", "5", "--signal", "1600", "--out",
+                 str(spb), "--truth", str(truth)]) == 0
+    assert main(["fit", "--in", str(spb), "--out", str(fits), "--flags"]) == 0
+    assert main(["fit", "--in", str(spb), "--out", str(fits2)]) == 0
+    got = read_params_csv(str(fits))
+    assert "flags" in got and int(((got["flags"] & 0x80) != 0).sum()) > 0
+    assert main(["assess", "--fits", str(fits), "--truth", str(truth), "--report", str(rep)]) == 0
+    assert main(["assess", "--fits", str(fits2), "--truth", str(truth), "--report", str(rep2)]) == 0
+    r, r2 = json.load(open(rep)), json.load(open(rep2))
+    assert r["iterations"]["no_improvement"] == int(((got["flags"] & 0x80) != 0).sum())
+    assert r2["iterations"]["no_improvement"] is None  # unavailable without the column, not a false 0
+    assert r["accuracy"] == r2["accuracy"]
