@@ -29,6 +29,101 @@ __host__ __device__ constexpr int init_buf_elems(int G, int N) {
   return ((G * N * (int)sizeof(PX) + 47) & ~15) / (int)sizeof(PX);
 }
 
+// A lane's column of the tame walk when the grid is no wider than the spot's lanes (W <= L, every
+// 2D grid of the fitter): column x, rows [y0, y1) (several row segments per column when W < L / 2),
+// with its neighbour offsets, 0/1 masks and window counts -- the geometry of sf_init_core.cuh's
+// init_scan_tame, computed once per kernel instead of once per spot.
+struct TameCol {
+  bool active;
+  int x, y0, y1, ol, orr;
+  float ml, mr, ci, ce, rci, rce;
+};
+
+template <int L>
+__device__ __forceinline__ TameCol tame_col(int W, int H, int gl) {
+  TameCol c;
+  int S = L / W;  // row segments per column
+  if (S > H) S = H;
+  c.x = gl % W;
+  const int seg = gl / W;
+  c.active = seg < S;
+  c.y0 = seg * H / S;
+  c.y1 = (seg + 1) * H / S;
+  c.ol = c.x > 0 ? -1 : 0;
+  c.orr = c.x < W - 1 ? 1 : 0;
+  c.ml = c.x > 0 ? 1.0f : 0.0f;
+  c.mr = c.x < W - 1 ? 1.0f : 0.0f;
+  const int cxi = 1 + (c.x > 0) + (c.x < W - 1);
+  c.ci = (float)(3 * cxi);
+  c.ce = (float)((H > 1 ? 2 : 1) * cxi);
+  c.rci = __frcp_rn(c.ci);
+  c.rce = __frcp_rn(c.ce);
+  return c;
+}
+
+// The tame walk of one column (arithmetic of sf_init_core.cuh:init_scan_tame, same values, same
+// first-maximum and minimum), which also checks the tame condition on every pixel it centres: the
+// walk runs speculatively and its result is used only when the whole spot turns out tame, so the
+// spot is read once for both.  Integer-valued pixels below 2^20 keep every partial sum exact in f32.
+template <typename PX>
+__device__ __forceinline__ void walk_tame(const PX* st, int W, int H, const TameCol& c, InitScan& a, bool& tame) {
+  using Acc = typename TameAcc<PX>::T;
+  const PX* col = st + c.x;
+  const Acc ml = (Acc)c.ml, mr = (Acc)c.mr;
+  bool tm = true;
+  auto chk = [&](PX raw) {
+    if constexpr (sizeof(PX) == 4) {  // u16 counts are tame by construction
+      const float v = (float)raw;
+      tm = tm && __float_as_uint(v) <= 0x49800000u && __fsub_rn(__fadd_rn(v, 8388608.0f), 8388608.0f) == v;
+    }
+  };
+  auto hsum = [&](int y) -> Acc {
+    const PX* r = col + y * W;
+    const PX v = r[0];
+    chk(v);
+    return (Acc)v + ml * (Acc)r[c.ol] + mr * (Acc)r[c.orr];
+  };
+  auto value = [&](int y, Acc sum) {
+    const bool edge = y == 0 || y == H - 1;  // count 1, 2, 3, 4, 6 or 9
+    return tame_div((float)sum, edge ? c.ce : c.ci, edge ? c.rce : c.rci);
+  };
+  const int y0 = c.y0, y1 = c.y1;
+  Acc prev = y0 > 0 ? hsum(y0 - 1) : (Acc)0;
+  Acc cur = hsum(y0);
+  float best = -1.0f;  // below every tame value
+  int brow = y0;
+  float lo = a.lo;
+  int y = y0;
+#pragma unroll 1
+  for (; y + 1 < y1; y += 2) {
+    const Acc n1 = hsum(y + 1);
+    const Acc n2 = y + 2 < H ? hsum(y + 2) : (Acc)0;
+    const float va = value(y, prev + cur + n1);
+    const float vb = value(y + 1, cur + n1 + n2);
+    const bool tb = vb > va;  // the pair's first maximum
+    const float vm = tb ? vb : va;
+    if (vm > best) {
+      best = vm;
+      brow = tb ? y + 1 : y;
+    }
+    lo = fminf(lo, fminf(va, vb));
+    prev = n1;
+    cur = n2;
+  }
+  if (y < y1) {
+    const Acc n1 = y + 1 < H ? hsum(y + 1) : (Acc)0;
+    const float va = value(y, prev + cur + n1);
+    if (va > best) {
+      best = va;
+      brow = y;
+    }
+    lo = fminf(lo, va);
+  }
+  a.key = key_max(a.key, scan_key(best, brow * W + c.x));
+  a.lo = lo;
+  tame = tame && tm;
+}
+
 template <int L, typename PX>
 __global__ void __launch_bounds__(32 * kInitWarps) init_kernel(const PX* __restrict__ images, int W, int H,
                                                               int64_t count, int P, double smin, double smax,
@@ -66,22 +161,36 @@ __global__ void __launch_bounds__(32 * kInitWarps) init_kernel(const PX* __restr
     }
     return (int)(((uintptr_t)src & 15) / sizeof(PX));
   };
+  // sigma(M) for every possible M, once per CTA (init_sigma: the same f64 ops, so the same floats)
+  float* sig_tab = reinterpret_cast<float*>(init_smem + (size_t)kInitWarps * 2 * be * sizeof(PX));
+  for (int m = threadIdx.x; m <= N; m += blockDim.x) sig_tab[m] = init_sigma(m, smin, smax);
+  __syncthreads();
+  const bool narrow = W <= L;  // every 2D grid: one column (segment) per lane, geometry hoisted
+  const TameCol tc = narrow ? tame_col<L>(W, H, sl) : TameCol{};
   int64_t t = (int64_t)blockIdx.x * kInitWarps + warp;
-  int off[2] = {0, 0};
-  if (t < ntask) off[0] = stage(t, 0);
+  int off0 = 0, off1 = 0;  // window offsets of the two staging buffers (registers, no local array)
+  if (t < ntask) off0 = stage(t, 0);
   cp_async_commit();
 #pragma unroll 1
   for (int i = 0; t < ntask; t += stride, ++i) {
     const int b = i & 1;
-    if (t + stride < ntask) off[b ^ 1] = stage(t + stride, b ^ 1);
+    if (t + stride < ntask) {
+      const int o = stage(t + stride, b ^ 1);
+      if (b) off0 = o;
+      else off1 = o;
+    }
     cp_async_commit();
     asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // this task's copies have landed
     __syncwarp();
     const int64_t spot = t * G + sub;
     const bool valid = spot < count;
-    const PX* sp = buf + b * be + off[b] + sub * N;
+    const PX* sp = buf + b * be + (b ? off1 : off0) + sub * N;
+    InitScan a;
+    scan_reset(a);
     bool tame = true;
-    if (valid) {
+    if (narrow) {  // speculative tame walk that checks tameness as it goes
+      if (valid && tc.active) walk_tame<PX>(sp, W, H, tc, a, tame);
+    } else if (valid) {
       for (int j = sl; j < N; j += L) {
         const float v = (float)sp[j];
         tame = tame && __float_as_uint(v) <= 0x49800000u && __fsub_rn(__fadd_rn(v, 8388608.0f), 8388608.0f) == v;
@@ -91,13 +200,13 @@ __global__ void __launch_bounds__(32 * kInitWarps) init_kernel(const PX* __restr
 #pragma unroll
     for (int o = 1; o < L; o <<= 1) tm &= __shfl_xor_sync(kFull, tm, o);
     tame = tm != 0;
-    InitScan a;
-    scan_reset(a);
     if (valid) {
-      if (tame)
-        init_scan_tame<L, PX>(sp, W, H, sl, a);
-      else
+      if (!tame) {  // the general f64 scan (rare: non-integer or large pixel values)
+        scan_reset(a);
         init_scan(sp, W, H, N, invW, sl, L, a);
+      } else if (!narrow) {
+        init_scan_tame<L, PX>(sp, W, H, sl, a);
+      }
     }
     scan_reduce<L>(a);
     int idx;
@@ -109,7 +218,7 @@ __global__ void __launch_bounds__(32 * kInitWarps) init_kernel(const PX* __restr
 #pragma unroll
     for (int o = 1; o < L; o <<= 1) m += __shfl_xor_sync(kFull, m, o);
     if (valid) {
-      const float sg = init_sigma(m, smin, smax);
+      const float sg = sig_tab[m];
       if (sl < P) {  // (x, y, sigma[, sigma]); P = 5 (explicit-5, internal): (x, y, sigma, alpha, beta)
         const int y = (int)(((float)idx + 0.5f) * invW);  // idx / W exactly (see init_smoothed)
         inits[spot * P + sl] = sl == 0 ? (float)(idx - y * W)
@@ -126,7 +235,9 @@ template <int L, typename PX>
 cudaError_t launch_init_l(const PX* images, int W, int H, int64_t count, int P, double smin, double smax,
                           float* inits, float* amps, cudaStream_t stream) {
   constexpr int G = 32 / L;
-  const size_t smem = (size_t)kInitWarps * 2 * init_buf_elems<PX>(G, W * H) * sizeof(PX);  // <= 66 KB
+  // staging buffers (<= 66 KB) + the sigma(M) table
+  const size_t smem = (size_t)kInitWarps * 2 * init_buf_elems<PX>(G, W * H) * sizeof(PX) +
+                      (size_t)(W * H + 1) * sizeof(float);
   auto kern = init_kernel<L, PX>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
