@@ -31,12 +31,12 @@ __host__ __device__ constexpr int init_buf_elems(int G, int N) {
 
 // A lane's column of the tame walk when the grid is no wider than the spot's lanes (W <= L, every
 // 2D grid of the fitter): column x, rows [y0, y1) (several row segments per column when W < L / 2),
-// with its neighbour offsets, 0/1 masks and window counts -- the geometry of sf_init_core.cuh's
+// with its window counts -- the geometry of sf_init_core.cuh's
 // init_scan_tame, computed once per kernel instead of once per spot.
 struct TameCol {
   bool active;
-  int x, y0, y1, ol, orr;
-  float ml, mr, ci, ce, rci, rce;
+  int x, y0, y1;
+  float ci, ce, rci, rce;
 };
 
 template <int L>
@@ -49,10 +49,6 @@ __device__ __forceinline__ TameCol tame_col(int W, int H, int gl) {
   c.active = seg < S;
   c.y0 = seg * H / S;
   c.y1 = (seg + 1) * H / S;
-  c.ol = c.x > 0 ? -1 : 0;
-  c.orr = c.x < W - 1 ? 1 : 0;
-  c.ml = c.x > 0 ? 1.0f : 0.0f;
-  c.mr = c.x < W - 1 ? 1.0f : 0.0f;
   const int cxi = 1 + (c.x > 0) + (c.x < W - 1);
   c.ci = (float)(3 * cxi);
   c.ce = (float)((H > 1 ? 2 : 1) * cxi);
@@ -61,67 +57,80 @@ __device__ __forceinline__ TameCol tame_col(int W, int H, int gl) {
   return c;
 }
 
-// The tame walk of one column (arithmetic of sf_init_core.cuh:init_scan_tame, same values, same
-// first-maximum and minimum), which also checks the tame condition on every pixel it centres: the
+// The tame walk of one column (the arithmetic of sf_init_core.cuh:init_scan_tame: same values, same
+// first maximum and minimum), which also checks the tame condition on every pixel it centres: the
 // walk runs speculatively and its result is used only when the whole spot turns out tame, so the
-// spot is read once for both.  Integer-valued pixels below 2^20 keep every partial sum exact in f32.
+// spot is read once for both.  Integer-valued pixels below 2^20 keep every partial sum exact in f32,
+// so the order of the three taps does not matter.  Neighbours are read at constant offsets -1 / +1
+// from the row pointer (the staging area has a guard in front, see init_kernel) and a missing one
+// (grid edge) is dropped by a select, never multiplied, so whatever lies there cannot leak in.  The
+// top and bottom grid rows (window count 2 cxi) are peeled off the interior loop (3 cxi).
 template <typename PX>
 __device__ __forceinline__ void walk_tame(const PX* st, int W, int H, const TameCol& c, InitScan& a, bool& tame) {
   using Acc = typename TameAcc<PX>::T;
-  const PX* col = st + c.x;
-  const Acc ml = (Acc)c.ml, mr = (Acc)c.mr;
-  bool tm = true;
-  auto chk = [&](PX raw) {
-    if constexpr (sizeof(PX) == 4) {  // u16 counts are tame by construction
-      const float v = (float)raw;
-      tm = tm && __float_as_uint(v) <= 0x49800000u && __fsub_rn(__fadd_rn(v, 8388608.0f), 8388608.0f) == v;
-    }
-  };
-  auto hsum = [&](int y) -> Acc {
-    const PX* r = col + y * W;
+  const bool hl = c.x > 0, hr = c.x < W - 1;
+  unsigned mx = 0u;   // max pixel bit pattern (negative, -0, inf, NaN and > 2^20 all exceed 0x49800000)
+  bool frac = false;  // some pixel is not an integer
+  auto hsum = [&](const PX* r) -> Acc {
     const PX v = r[0];
-    chk(v);
-    return (Acc)v + ml * (Acc)r[c.ol] + mr * (Acc)r[c.orr];
-  };
-  auto value = [&](int y, Acc sum) {
-    const bool edge = y == 0 || y == H - 1;  // count 1, 2, 3, 4, 6 or 9
-    return tame_div((float)sum, edge ? c.ce : c.ci, edge ? c.rce : c.rci);
-  };
-  const int y0 = c.y0, y1 = c.y1;
-  Acc prev = y0 > 0 ? hsum(y0 - 1) : (Acc)0;
-  Acc cur = hsum(y0);
-  float best = -1.0f;  // below every tame value
-  int brow = y0;
-  float lo = a.lo;
-  int y = y0;
-#pragma unroll 1
-  for (; y + 1 < y1; y += 2) {
-    const Acc n1 = hsum(y + 1);
-    const Acc n2 = y + 2 < H ? hsum(y + 2) : (Acc)0;
-    const float va = value(y, prev + cur + n1);
-    const float vb = value(y + 1, cur + n1 + n2);
-    const bool tb = vb > va;  // the pair's first maximum
-    const float vm = tb ? vb : va;
-    if (vm > best) {
-      best = vm;
-      brow = tb ? y + 1 : y;
+    if constexpr (sizeof(PX) == 4) {  // u16 counts are tame by construction
+      const float f = (float)v;
+      mx = max(mx, __float_as_uint(f));
+      frac |= __fsub_rn(__fadd_rn(f, 8388608.0f), 8388608.0f) != f;
     }
-    lo = fminf(lo, fminf(va, vb));
-    prev = n1;
-    cur = n2;
-  }
-  if (y < y1) {
-    const Acc n1 = y + 1 < H ? hsum(y + 1) : (Acc)0;
-    const float va = value(y, prev + cur + n1);
-    if (va > best) {
-      best = va;
+    const Acc l = (Acc)r[-1], rr = (Acc)r[1];
+    return ((Acc)v + (hl ? l : (Acc)0)) + (hr ? rr : (Acc)0);
+  };
+  float best = -1.0f;  // below every tame value
+  int brow = c.y0;
+  float lo = a.lo;
+  auto take = [&](float v, int y) {
+    if (v > best) {  // rows ascend: a strict ">" keeps the column's first maximum
+      best = v;
       brow = y;
     }
-    lo = fminf(lo, va);
+    lo = fminf(lo, v);
+  };
+  const PX* p = st + c.x + c.y0 * W;  // row y
+  int y = c.y0;
+  Acc prev = y > 0 ? hsum(p - W) : (Acc)0;
+  Acc cur = hsum(p);
+  if (y == 0) {  // top grid row
+    const Acc nx = H > 1 ? hsum(p + W) : (Acc)0;
+    take(tame_div((float)(prev + cur + nx), c.ce, c.rce), 0);
+    prev = cur;
+    cur = nx;
+    p += W;
+    ++y;
   }
+  const int yi = c.y1 < H - 1 ? c.y1 : H - 1;  // interior rows [y, yi): row y + 1 exists
+#pragma unroll 2
+  for (; y < yi; ++y) {
+    const Acc nx = hsum(p + W);
+    take(tame_div((float)(prev + cur + nx), c.ci, c.rci), y);
+    prev = cur;
+    cur = nx;
+    p += W;
+  }
+  if (y < c.y1) take(tame_div((float)(prev + cur), c.ce, c.rce), y);  // bottom grid row (y = H - 1 > 0)
   a.key = key_max(a.key, scan_key(best, brow * W + c.x));
   a.lo = lo;
-  tame = tame && tm;
+  if constexpr (sizeof(PX) == 4) tame = tame && mx <= 0x49800000u && !frac;
+}
+
+// M of a tame spot over the lane's column segment (init_count_tame's test, g >= floor(thr) + 1, with
+// the threshold clamped the same way): one load, one compare and one add per pixel, pointer stepping.
+template <typename PX>
+__device__ __forceinline__ int count_column(const PX* st, int W, const TameCol& c, double thr) {
+  double t = floor(thr) + 1.0;
+  t = t < -1.0 ? -1.0 : (t > 2097152.0 ? 2097152.0 : t);
+  using Acc = typename TameAcc<PX>::T;
+  const Acc tt = (Acc)t;
+  const PX* p = st + c.x + c.y0 * W;
+  int m = 0;
+#pragma unroll 4
+  for (int y = c.y0; y < c.y1; ++y, p += W) m += ((Acc)p[0] >= tt) ? 1 : 0;
+  return m;
 }
 
 template <int L, typename PX>
@@ -134,7 +143,9 @@ __global__ void __launch_bounds__(32 * kInitWarps) init_kernel(const PX* __restr
   const int sub = lane / L, sl = lane % L;  // spot of the warp's G, lane within the spot
   const int N = W * H;
   const int be = init_buf_elems<PX>(G, N);
-  PX* buf = reinterpret_cast<PX*>(init_smem) + (size_t)warp * 2 * be;
+  // 16-byte guard in front of the staging buffers: the tame walk reads a row's left neighbour at a
+  // constant -1 offset (and drops it at the grid edge), so the first spot of warp 0 reads inside smem
+  PX* buf = reinterpret_cast<PX*>(init_smem + 16) + (size_t)warp * 2 * be;
   const float invW = 1.0f / (float)W;
   const int64_t ntask = (count + G - 1) / G;
   const int64_t stride = (int64_t)gridDim.x * kInitWarps;
@@ -162,7 +173,7 @@ __global__ void __launch_bounds__(32 * kInitWarps) init_kernel(const PX* __restr
     return (int)(((uintptr_t)src & 15) / sizeof(PX));
   };
   // sigma(M) for every possible M, once per CTA (init_sigma: the same f64 ops, so the same floats)
-  float* sig_tab = reinterpret_cast<float*>(init_smem + (size_t)kInitWarps * 2 * be * sizeof(PX));
+  float* sig_tab = reinterpret_cast<float*>(init_smem + 16 + (size_t)kInitWarps * 2 * be * sizeof(PX));
   for (int m = threadIdx.x; m <= N; m += blockDim.x) sig_tab[m] = init_sigma(m, smin, smax);
   __syncthreads();
   const bool narrow = W <= L;  // every 2D grid: one column (segment) per lane, geometry hoisted
@@ -214,7 +225,12 @@ __global__ void __launch_bounds__(32 * kInitWarps) init_kernel(const PX* __restr
     double thr;
     init_finish(a, idx, alpha, beta, thr);
     int m = 0;
-    if (valid) m = tame ? init_count_tame(sp, N, thr, sl, L) : init_count(sp, N, thr, sl, L);
+    if (valid) {
+      if (tame && narrow)
+        m = tc.active ? count_column(sp, W, tc, thr) : 0;
+      else
+        m = tame ? init_count_tame(sp, N, thr, sl, L) : init_count(sp, N, thr, sl, L);
+    }
 #pragma unroll
     for (int o = 1; o < L; o <<= 1) m += __shfl_xor_sync(kFull, m, o);
     if (valid) {
@@ -236,7 +252,7 @@ cudaError_t launch_init_l(const PX* images, int W, int H, int64_t count, int P, 
                           float* inits, float* amps, cudaStream_t stream) {
   constexpr int G = 32 / L;
   // staging buffers (<= 66 KB) + the sigma(M) table
-  const size_t smem = (size_t)kInitWarps * 2 * init_buf_elems<PX>(G, W * H) * sizeof(PX) +
+  const size_t smem = 16 + (size_t)kInitWarps * 2 * init_buf_elems<PX>(G, W * H) * sizeof(PX) +
                       (size_t)(W * H + 1) * sizeof(float);
   auto kern = init_kernel<L, PX>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
