@@ -345,6 +345,7 @@ struct HostJob {
   float *par, *alpha, *beta, *nchi2;
   uint8_t *status, *iters;
   bool pinned_in, pinned_out;
+  int copy_threads = 1;  // host threads for staging pageable input (par_memcpy)
   // results
   unsigned long long evals[3] = {0, 0, 0};
   double h2d_ms = 0, kernel_ms = 0, d2h_ms = 0;
@@ -352,6 +353,26 @@ struct HostJob {
   int rc = 0;
   std::string err;
 };
+
+// Pageable host input is staged into pinned buffers by the CPU.  One thread copies ~10 GB/s, far
+// below PCIe (~53 GB/s), so large chunks are copied by copy_threads threads (the host's cores split
+// over the devices of the call; SPOTFIT_COPY_THREADS overrides).
+void par_memcpy(void* dst, const void* src, size_t bytes, int threads) {
+  constexpr size_t kPiece = 4u << 20;
+  const int T = (int)std::min<size_t>((size_t)std::max(1, threads), (bytes + kPiece - 1) / kPiece);
+  if (T <= 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  const size_t per = ((bytes + T - 1) / T + 63) & ~(size_t)63;
+  std::vector<std::thread> th;
+  for (int t = 1; t < T; ++t) {
+    const size_t a = std::min(bytes, per * t), b = std::min(bytes, per * (t + 1));
+    if (b > a) th.emplace_back([=] { std::memcpy((char*)dst + a, (const char*)src + a, b - a); });
+  }
+  std::memcpy(dst, src, std::min(bytes, per));
+  for (auto& x : th) x.join();
+}
 
 void copy_out_staged(Slot& s, HostJob& j) {
   if (!s.pending) return;
@@ -437,7 +458,7 @@ int run_shard(int dev, HostJob& j) {
     const void* src_img = j.images16 ? (const void*)(j.images16 + lo * N) : (const void*)(j.images + lo * N);
     const float* src_init = j.inits ? j.inits + lo * P : nullptr;  // NULL: the fit kernel estimates them
     if (!j.pinned_in) {
-      std::memcpy(s.h_in, src_img, n * N * px_bytes);
+      par_memcpy(s.h_in, src_img, n * N * px_bytes, j.copy_threads);
       if (src_init) std::memcpy(s.h_in + s.cap_spots * N, src_init, n * P * sizeof(float));
       src_img = s.h_in;
       if (src_init) src_init = s.h_in + s.cap_spots * N;
@@ -897,6 +918,9 @@ static int fit_batch_impl(const float* images, const uint16_t* images16, int32_t
                        is_pinned_ptr(out_nchi2) && is_pinned_ptr(out_status) && is_pinned_ptr(out_iters);
   const int nd = (int)devs.size();
   std::vector<HostJob> jobs(nd);
+  int copy_threads = (int)std::thread::hardware_concurrency() / nd;
+  if (const char* e = std::getenv("SPOTFIT_COPY_THREADS")) copy_threads = (int)std::strtol(e, nullptr, 10);
+  copy_threads = std::max(1, std::min(copy_threads, 16));
   for (int d = 0; d < nd; ++d) {
     HostJob& j = jobs[d];
     j.images = images;
@@ -915,6 +939,7 @@ static int fit_batch_impl(const float* images, const uint16_t* images16, int32_t
     j.iters = out_iters;
     j.pinned_in = pin_in;
     j.pinned_out = pin_out;
+    j.copy_threads = copy_threads;
   }
   std::vector<std::thread> th;
   for (int d = 1; d < nd; ++d)
