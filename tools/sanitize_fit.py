@@ -41,4 +41,28 @@ for W, H in ((15, 15), (21, 21), (32, 32)):
     rec = sf.evaluate_batch(im.reshape(40, -1), tr[:, :3], W, H)
     dev = sf.simulate_batch_device(sf.SimConfig(width=W, height=H, count=40, seed=5))
     torch.cuda.synchronize()
+# the standalone initializer on every geometry family of its column walk (one column per lane, several
+# row segments per column, a 1-row grid, a wide grid with several columns per lane) and on non-integer
+# pixels (general path), against the oracle; the fused initializer (inits = None) and the model functions
+for W, H in ((15, 15), (5, 9), (1, 7), (9, 1), (40, 1), (13, 10), (32, 32)):
+    im, _ = sf.simulate_batch(sf.SimConfig(width=W, height=H, count=37, seed=W + 7 * H))
+    im = im.reshape(37, -1)
+    im[5] += 0.25  # one non-tame spot
+    got, _ = sf.estimate_initial_batch(im, 3, grid=sf.PixelGrid(W, H))
+    want, _ = oinit.estimate_initial_batch(im, W, H, 0.3, float(max(W, H)), 3)
+    same = np.array_equal(got.view(np.uint32), np.asarray(want, np.float32).view(np.uint32))
+    ok &= same
+    print(f"initializer {W}x{H}: {'ok' if same else 'MISMATCH'}", flush=True)
+    sf.fit_batch(im, grid=sf.PixelGrid(W, H))  # fused initializer + fit
+    torch.cuda.synchronize()
+from paper_2106_02045_b200 import model as sfm  # noqa: E402
+
+g = sfm.SpotImage.from_array(np.float32(np.random.default_rng(1).poisson(20.0, (9, 9))))
+shape = sfm.ShapeParams(4.0, 4.0, 1.5)
+f, fgrad = sfm.profile_and_gradient(shape, g.grid)
+amps, sums = sfm.alpha_beta(f, g)
+gs = sfm.gradient_sums(f, fgrad, g, sums)
+cg = sfm.coefficient_gradients(sums, gs, amps)
+sfm.chi_gradient(g, f, fgrad, amps, cg)
+sfm.chi_squared(g, f, amps)
 print("SANITIZE_FIT", "ok" if ok else "FAIL")
