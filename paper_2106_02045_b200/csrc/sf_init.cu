@@ -39,16 +39,25 @@ struct TameCol {
   float ci, ce, rci, rce;
 };
 
+// Column k (0 or 1) of lane gl: when W <= L one column per lane, split into S row segments when
+// W < L / 2; when L < W <= 2L two full-height columns per lane (x = gl and gl + L).
 template <int L>
-__device__ __forceinline__ TameCol tame_col(int W, int H, int gl) {
+__device__ __forceinline__ TameCol tame_col(int W, int H, int gl, int k) {
   TameCol c;
-  int S = L / W;  // row segments per column
-  if (S > H) S = H;
-  c.x = gl % W;
-  const int seg = gl / W;
-  c.active = seg < S;
-  c.y0 = seg * H / S;
-  c.y1 = (seg + 1) * H / S;
+  if (W <= L) {
+    int S = L / W;  // row segments per column
+    if (S > H) S = H;
+    c.x = gl % W;
+    const int seg = gl / W;
+    c.active = k == 0 && seg < S;
+    c.y0 = seg * H / S;
+    c.y1 = (seg + 1) * H / S;
+  } else {
+    c.x = gl + k * L;
+    c.active = c.x < W;
+    c.y0 = 0;
+    c.y1 = H;
+  }
   const int cxi = 1 + (c.x > 0) + (c.x < W - 1);
   c.ci = (float)(3 * cxi);
   c.ce = (float)((H > 1 ? 2 : 1) * cxi);
@@ -57,21 +66,29 @@ __device__ __forceinline__ TameCol tame_col(int W, int H, int gl) {
   return c;
 }
 
-// The tame walk of one column (the arithmetic of sf_init_core.cuh:init_scan_tame: same values, same
-// first maximum and minimum), which also checks the tame condition on every pixel it centres: the
-// walk runs speculatively and its result is used only when the whole spot turns out tame, so the
-// spot is read once for both.  Integer-valued pixels below 2^20 keep every partial sum exact in f32,
-// so the order of the three taps does not matter.  Neighbours are read at constant offsets -1 / +1
-// from the row pointer (the staging area has a guard in front, see init_kernel) and a missing one
-// (grid edge) is dropped by a select, never multiplied, so whatever lies there cannot leak in.  The
-// top and bottom grid rows (window count 2 cxi) are peeled off the interior loop (3 cxi).
-template <typename PX>
-__device__ __forceinline__ void walk_tame(const PX* st, int W, int H, const TameCol& c, InitScan& a, bool& tame) {
+// The tame walk of NC columns in lockstep (the arithmetic of sf_init_core.cuh:init_scan_tame: same
+// values, same first maximum and minimum; NC = 2 gives the walk two independent chains), which also
+// checks the tame condition on every pixel it centres: the walk runs speculatively and its result is
+// used only when the whole spot turns out tame, so the spot is read once for both.  Integer-valued
+// pixels below 2^20 keep every partial sum exact in f32, so the order of the three taps does not
+// matter.  Neighbours are read at constant offsets -1 / +1 from the row pointer (the staging area has
+// a guard in front, see init_kernel) and a missing one (grid edge) is dropped by a select, never
+// multiplied, so whatever lies there cannot leak in.  The top and bottom grid rows (window count
+// 2 cxi) are peeled off the interior loop (3 cxi).  All columns share the rows [y0, y1) of cs[0].
+template <int NC, typename PX>
+__device__ __forceinline__ void walk_tame(const PX* st, int W, int H, const TameCol (&cs)[NC], InitScan& a,
+                                          bool& tame) {
   using Acc = typename TameAcc<PX>::T;
-  const bool hl = c.x > 0, hr = c.x < W - 1;
+  bool hl[NC], hr[NC];
+  const PX* p[NC];
+  Acc prev[NC], cur[NC];
+  float best[NC];
+  int brow[NC];
   unsigned mx = 0u;   // max pixel bit pattern (negative, -0, inf, NaN and > 2^20 all exceed 0x49800000)
   bool frac = false;  // some pixel is not an integer
-  auto hsum = [&](const PX* r) -> Acc {
+  float lo = a.lo;
+  const int y0 = cs[0].y0, y1 = cs[0].y1;
+  auto hsum = [&](int k, const PX* r) -> Acc {
     const PX v = r[0];
     if constexpr (sizeof(PX) == 4) {  // u16 counts are tame by construction
       const float f = (float)v;
@@ -79,62 +96,99 @@ __device__ __forceinline__ void walk_tame(const PX* st, int W, int H, const Tame
       frac |= __fsub_rn(__fadd_rn(f, 8388608.0f), 8388608.0f) != f;
     }
     const Acc l = (Acc)r[-1], rr = (Acc)r[1];
-    return ((Acc)v + (hl ? l : (Acc)0)) + (hr ? rr : (Acc)0);
+    return ((Acc)v + (hl[k] ? l : (Acc)0)) + (hr[k] ? rr : (Acc)0);
   };
-  float best = -1.0f;  // below every tame value
-  int brow = c.y0;
-  float lo = a.lo;
-  auto take = [&](float v, int y) {
-    if (v > best) {  // rows ascend: a strict ">" keeps the column's first maximum
-      best = v;
-      brow = y;
+  auto take = [&](int k, float v, int y) {
+    if (v > best[k]) {  // rows ascend: a strict ">" keeps the column's first maximum
+      best[k] = v;
+      brow[k] = y;
     }
     lo = fminf(lo, v);
   };
-  const PX* p = st + c.x + c.y0 * W;  // row y
-  int y = c.y0;
-  Acc prev = y > 0 ? hsum(p - W) : (Acc)0;
-  Acc cur = hsum(p);
+#pragma unroll
+  for (int k = 0; k < NC; ++k) {
+    hl[k] = cs[k].x > 0;
+    hr[k] = cs[k].x < W - 1;
+    p[k] = st + cs[k].x + y0 * W;
+    best[k] = -1.0f;  // below every tame value
+    brow[k] = y0;
+    prev[k] = y0 > 0 ? hsum(k, p[k] - W) : (Acc)0;
+    cur[k] = hsum(k, p[k]);
+  }
+  int y = y0;
   if (y == 0) {  // top grid row
-    const Acc nx = H > 1 ? hsum(p + W) : (Acc)0;
-    take(tame_div((float)(prev + cur + nx), c.ce, c.rce), 0);
-    prev = cur;
-    cur = nx;
-    p += W;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      const Acc nx = H > 1 ? hsum(k, p[k] + W) : (Acc)0;
+      take(k, tame_div((float)(prev[k] + cur[k] + nx), cs[k].ce, cs[k].rce), 0);
+      prev[k] = cur[k];
+      cur[k] = nx;
+      p[k] += W;
+    }
     ++y;
   }
-  const int yi = c.y1 < H - 1 ? c.y1 : H - 1;  // interior rows [y, yi): row y + 1 exists
+  const int yi = y1 < H - 1 ? y1 : H - 1;  // interior rows [y, yi): row y + 1 exists
 #pragma unroll 2
   for (; y < yi; ++y) {
-    const Acc nx = hsum(p + W);
-    take(tame_div((float)(prev + cur + nx), c.ci, c.rci), y);
-    prev = cur;
-    cur = nx;
-    p += W;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      const Acc nx = hsum(k, p[k] + W);
+      take(k, tame_div((float)(prev[k] + cur[k] + nx), cs[k].ci, cs[k].rci), y);
+      prev[k] = cur[k];
+      cur[k] = nx;
+      p[k] += W;
+    }
   }
-  if (y < c.y1) take(tame_div((float)(prev + cur), c.ce, c.rce), y);  // bottom grid row (y = H - 1 > 0)
-  a.key = key_max(a.key, scan_key(best, brow * W + c.x));
+  if (y < y1) {  // bottom grid row (y = H - 1 > 0)
+#pragma unroll
+    for (int k = 0; k < NC; ++k) take(k, tame_div((float)(prev[k] + cur[k]), cs[k].ce, cs[k].rce), y);
+  }
+  unsigned long long key = a.key;
+#pragma unroll
+  for (int k = 0; k < NC; ++k) key = key_max(key, scan_key(best[k], brow[k] * W + cs[k].x));
+  a.key = key;
   a.lo = lo;
   if constexpr (sizeof(PX) == 4) tame = tame && mx <= 0x49800000u && !frac;
 }
 
-// M of a tame spot over the lane's column segment (init_count_tame's test, g >= floor(thr) + 1, with
-// the threshold clamped the same way): one load, one compare and one add per pixel, pointer stepping.
-template <typename PX>
-__device__ __forceinline__ int count_column(const PX* st, int W, const TameCol& c, double thr) {
+// M of a tame spot over the lane's NC columns (init_count_tame's test, g >= floor(thr) + 1, with the
+// threshold clamped the same way), in lockstep; column k counts only when live[k].
+template <int NC, typename PX>
+__device__ __forceinline__ int count_columns(const PX* st, int W, const TameCol (&cs)[NC], const bool (&live)[NC],
+                                             double thr) {
   double t = floor(thr) + 1.0;
   t = t < -1.0 ? -1.0 : (t > 2097152.0 ? 2097152.0 : t);
   using Acc = typename TameAcc<PX>::T;
   const Acc tt = (Acc)t;
-  const PX* p = st + c.x + c.y0 * W;
-  int m = 0;
+  // f32 tame pixels are non-negative, so float order is the order of the bit patterns: compare bits
+  // (a threshold <= 0 counts every pixel: +0 is the smallest tame bit pattern)
+  const unsigned tb = __float_as_uint(fmaxf((float)t, 0.0f));
+  const PX* p[NC];
+  int m[NC];
+#pragma unroll
+  for (int k = 0; k < NC; ++k) {
+    p[k] = st + cs[k].x + cs[0].y0 * W;
+    m[k] = 0;
+  }
 #pragma unroll 4
-  for (int y = c.y0; y < c.y1; ++y, p += W) m += ((Acc)p[0] >= tt) ? 1 : 0;
-  return m;
+  for (int y = cs[0].y0; y < cs[0].y1; ++y) {
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      if constexpr (sizeof(PX) == 4)
+        m[k] += (__float_as_uint((float)p[k][0]) >= tb) ? 1 : 0;
+      else
+        m[k] += ((Acc)p[k][0] >= tt) ? 1 : 0;
+      p[k] += W;
+    }
+  }
+  int r = 0;
+#pragma unroll
+  for (int k = 0; k < NC; ++k) r += live[k] ? m[k] : 0;
+  return r;
 }
 
 template <int L, typename PX>
-__global__ void __launch_bounds__(32 * kInitWarps) init_kernel(const PX* __restrict__ images, int W, int H,
+__global__ void __launch_bounds__(32 * kInitWarps, 3) init_kernel(const PX* __restrict__ images, int W, int H,
                                                               int64_t count, int P, double smin, double smax,
                                                               float* __restrict__ inits, float* __restrict__ amps) {
   constexpr int G = 32 / L;
@@ -158,6 +212,13 @@ __global__ void __launch_bounds__(32 * kInitWarps) init_kernel(const PX* __restr
     if (e0 > ((hi + 15) & ~(uintptr_t)15)) e0 = (hi + 15) & ~(uintptr_t)15;
     const int nck = (int)((e0 - a0) >> 4);
     PX* dst = buf + b * be;
+    if (a0 >= lo && e0 <= hi) {  // the whole window inside the caller's array: 16-byte copies only
+      const char* s0 = reinterpret_cast<const char*>(a0);
+      float* d0 = reinterpret_cast<float*>(dst);
+#pragma unroll 4
+      for (int c = lane; c < nck; c += 32) cp_async16(d0 + 4 * c, s0 + 16 * c);
+      return (int)(((uintptr_t)src & 15) / sizeof(PX));
+    }
     for (int c = lane; c < nck; c += 32) {
       const uintptr_t cs = a0 + 16 * (uintptr_t)c;
       float* d = reinterpret_cast<float*>(dst) + 4 * c;
@@ -176,8 +237,15 @@ __global__ void __launch_bounds__(32 * kInitWarps) init_kernel(const PX* __restr
   float* sig_tab = reinterpret_cast<float*>(init_smem + 16 + (size_t)kInitWarps * 2 * be * sizeof(PX));
   for (int m = threadIdx.x; m <= N; m += blockDim.x) sig_tab[m] = init_sigma(m, smin, smax);
   __syncthreads();
-  const bool narrow = W <= L;  // every 2D grid: one column (segment) per lane, geometry hoisted
-  const TameCol tc = narrow ? tame_col<L>(W, H, sl) : TameCol{};
+  // every 2D grid (W <= 2L): at most two columns per lane, geometry hoisted out of the spot loop
+  const bool narrow = W <= 2 * L;
+  const bool two = narrow && W > L;  // two full-height columns per lane, walked in lockstep
+  const TameCol tc0 = narrow ? tame_col<L>(W, H, sl, 0) : TameCol{};
+  TameCol tcs[2] = {tc0, narrow ? tame_col<L>(W, H, sl, 1) : TameCol{}};
+  const bool live[2] = {tc0.active, tcs[1].active};
+  if (!tcs[1].active) tcs[1] = tc0;  // a lane without a second column repeats its first (same values)
+  const TameCol one[1] = {tc0};
+  const bool live1[1] = {true};
   int64_t t = (int64_t)blockIdx.x * kInitWarps + warp;
   int off0 = 0, off1 = 0;  // window offsets of the two staging buffers (registers, no local array)
   if (t < ntask) off0 = stage(t, 0);
@@ -200,7 +268,12 @@ __global__ void __launch_bounds__(32 * kInitWarps) init_kernel(const PX* __restr
     scan_reset(a);
     bool tame = true;
     if (narrow) {  // speculative tame walk that checks tameness as it goes
-      if (valid && tc.active) walk_tame<PX>(sp, W, H, tc, a, tame);
+      if (valid && tc0.active) {
+        if (two)
+          walk_tame<2, PX>(sp, W, H, tcs, a, tame);
+        else
+          walk_tame<1, PX>(sp, W, H, one, a, tame);
+      }
     } else if (valid) {
       for (int j = sl; j < N; j += L) {
         const float v = (float)sp[j];
@@ -227,7 +300,7 @@ __global__ void __launch_bounds__(32 * kInitWarps) init_kernel(const PX* __restr
     int m = 0;
     if (valid) {
       if (tame && narrow)
-        m = tc.active ? count_column(sp, W, tc, thr) : 0;
+        m = !tc0.active ? 0 : (two ? count_columns<2, PX>(sp, W, tcs, live, thr) : count_columns<1, PX>(sp, W, one, live1, thr));
       else
         m = tame ? init_count_tame(sp, N, thr, sl, L) : init_count(sp, N, thr, sl, L);
     }
@@ -274,11 +347,13 @@ template <typename PX>
 cudaError_t launch_init_px(const PX* images, int W, int H, int64_t count, int P, double sigma_min, double sigma_max,
                            float* inits, float* amps, cudaStream_t stream) {
   if (count <= 0) return cudaSuccess;
-  // L lanes per spot: enough to give every lane a column, and G * N <= 1024 pixels per warp buffer
   const int N = W * H;
-  if (W > 16 || N > 512) return launch_init_l<32, PX>(images, W, H, count, P, sigma_min, sigma_max, inits, amps, stream);
-  if (W > 8 || N > 256) return launch_init_l<16, PX>(images, W, H, count, P, sigma_min, sigma_max, inits, amps, stream);
-  return launch_init_l<8, PX>(images, W, H, count, P, sigma_min, sigma_max, inits, amps, stream);
+  // L lanes per spot, G = 32 / L spots per warp: the fewest lanes that leave each lane at most two
+  // columns (W <= 2L) with G * N <= 1024 pixels per warp buffer; more spots per warp share the
+  // per-spot reductions and bookkeeping
+  if (W <= 16 && N <= 256) return launch_init_l<8, PX>(images, W, H, count, P, sigma_min, sigma_max, inits, amps, stream);
+  if (W <= 32 && N <= 512) return launch_init_l<16, PX>(images, W, H, count, P, sigma_min, sigma_max, inits, amps, stream);
+  return launch_init_l<32, PX>(images, W, H, count, P, sigma_min, sigma_max, inits, amps, stream);
 }
 
 cudaError_t launch_estimate_initial(const float* images, int W, int H, int64_t count, int P, double sigma_min,
