@@ -299,6 +299,14 @@ const char* sf_csv_last_error(void);
  */
 int sf_shard_range(int64_t count, int32_t shard, int32_t n_shards, int64_t* lo, int64_t* hi);
 
+/*
+ * sf_debug_narrow_u16 -- diagnostic: the host pipeline's lossless narrowing of f32 pixel chunks for
+ * the PCIe leg (sf_fit_batch sends a pageable f32 chunk as u16 when every pixel is an integer in
+ * [0, 65535] with a clear sign bit; SPOTFIT_NARROW=0 disables it, =2 applies it to pinned input too).  Returns 1 if all n values narrowed (dst
+ * holds them), 0 if some value did not, -1 on bad arguments.  Host-only.
+ */
+int sf_debug_narrow_u16(const float* src, int64_t n, uint16_t* dst, int32_t threads);
+
 int sf_device_count(void);
 const char* sf_last_error(void);
 int sf_version(void);

@@ -222,6 +222,7 @@ struct Slot {
   uint8_t* d_st = nullptr;
   uint8_t* d_it = nullptr;
   float* h_in = nullptr;   // pinned staging (pageable callers): images then inits
+  uint16_t* h_in16 = nullptr;  // pinned u16 staging: integer-valued f32 chunks narrowed for the PCIe leg
   float* h_out = nullptr;  // pinned staging: params, alpha, beta, nchi2, status, iters
   size_t cap_spots = 0, cap_npix = 0;
   bool pending = false;  // staged results of a finished chunk waiting to be copied out
@@ -249,15 +250,16 @@ DevCtx* ctx_for(int dev) {
 void free_slot_buffers(Slot& s) {
   cudaFree(s.d_img); cudaFree(s.d_img16); cudaFree(s.d_init); cudaFree(s.d_par); cudaFree(s.d_a); cudaFree(s.d_b); cudaFree(s.d_c);
   cudaFree(s.d_st); cudaFree(s.d_it);
-  cudaFreeHost(s.h_in); cudaFreeHost(s.h_out);
+  cudaFreeHost(s.h_in); cudaFreeHost(s.h_out); cudaFreeHost(s.h_in16);
   s.d_img = s.d_init = s.d_par = s.d_a = s.d_b = s.d_c = nullptr;
   s.d_img16 = nullptr;
   s.d_st = s.d_it = nullptr;
   s.h_in = s.h_out = nullptr;
+  s.h_in16 = nullptr;
   s.cap_spots = 0;
 }
 
-int ensure_ctx(DevCtx& c, int dev, size_t spots, int npix, int P, bool staging) {
+int ensure_ctx(DevCtx& c, int dev, size_t spots, int npix, int P, bool staging, bool narrow) {
   if (!c.init) {
     SF_CUDA(cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev));
     for (auto& s : c.slot) {
@@ -268,7 +270,8 @@ int ensure_ctx(DevCtx& c, int dev, size_t spots, int npix, int P, bool staging) 
     c.init = true;
   }
   for (auto& s : c.slot) {
-    const bool grow = s.cap_spots < spots || s.cap_npix < (size_t)npix || (staging && s.h_in == nullptr);
+    const bool grow = s.cap_spots < spots || s.cap_npix < (size_t)npix || (staging && s.h_in == nullptr) ||
+                      (narrow && s.h_in16 == nullptr);
     if (!grow) continue;
     free_slot_buffers(s);
     SF_CUDA(cudaMalloc(&s.d_img, spots * npix * sizeof(float)));
@@ -284,6 +287,7 @@ int ensure_ctx(DevCtx& c, int dev, size_t spots, int npix, int P, bool staging) 
       SF_CUDA(cudaHostAlloc(&s.h_in, spots * (npix + kMaxP) * sizeof(float), cudaHostAllocPortable));
       SF_CUDA(cudaHostAlloc(&s.h_out, spots * (kMaxP + 3 + 1) * sizeof(float), cudaHostAllocPortable));
     }
+    if (narrow) SF_CUDA(cudaHostAlloc(&s.h_in16, spots * npix * sizeof(uint16_t), cudaHostAllocPortable));
     s.cap_spots = spots;
     s.cap_npix = npix;
   }
@@ -430,7 +434,17 @@ int run_shard(int dev, HostJob& j) {
   int64_t chunk = 0;
   for (const auto& ch : chunks) chunk = std::max(chunk, ch.second);
   const bool staging = !(j.pinned_in && j.pinned_out);
-  if (ensure_ctx(*c, dev, (size_t)chunk, N, P, staging) != 0) return -1;
+  // Pageable f32 chunks whose pixels are all integers in [0, 65535] cross PCIe as u16
+  // (sf_host_narrow.cpp): the CPU has to touch pageable pixels anyway (staging copy), and narrowing
+  // writes half the bytes.  Pinned f32 input is not narrowed: its H2D is a DMA straight from the
+  // caller's buffer at ~53 GB/s, faster than the host narrows (~45 GB/s of input on 16 cores,
+  // profiles/r02_bench_e2e_narrow.txt).  SPOTFIT_NARROW=0 disables, =2 narrows pinned input as well.
+  static const int narrow_env = [] {
+    const char* e = std::getenv("SPOTFIT_NARROW");
+    return e ? (int)std::strtol(e, nullptr, 10) : 1;
+  }();
+  const bool narrow = narrow_env > 0 && !j.images16 && j.images != nullptr && (!j.pinned_in || narrow_env > 1);
+  if (ensure_ctx(*c, dev, (size_t)chunk, N, P, staging, narrow) != 0) return -1;
   SF_CUDA(cudaMemsetAsync(c->d_evals, 0, 3 * sizeof(unsigned long long), c->slot[0].stream));
   SF_CUDA(cudaStreamSynchronize(c->slot[0].stream));
   // SPOTFIT_TRACE=1: per-chunk device timeline on stderr (diagnostic; tools/e2e_sweep.py)
@@ -448,27 +462,35 @@ int run_shard(int dev, HostJob& j) {
     Slot& s = c->slot[ci % kStreams];
     const int64_t lo = j.lo + chunks[ci].first;
     const int64_t n = chunks[ci].second;
-    if (staging) {  // the slot's previous chunk must be finished before its staging is reused
+    if (staging || narrow) {  // the slot's previous chunk must be finished before its staging is reused
       SF_CUDA(cudaEventSynchronize(s.ev[3]));
-      copy_out_staged(s, j);
+      if (staging) copy_out_staged(s, j);
     }
     SF_CUDA(cudaEventRecord(s.ev[0], s.stream));
     SF_CUDA(mark(s.stream));
-    const size_t px_bytes = j.images16 ? sizeof(uint16_t) : sizeof(float);
-    const void* src_img = j.images16 ? (const void*)(j.images16 + lo * N) : (const void*)(j.images + lo * N);
+    // this chunk as u16: 16-bit input, or f32 input whose pixels all narrow exactly
+    const bool u16 = j.images16 != nullptr ||
+                     (narrow && sf::par_narrow_u16(s.h_in16, j.images + lo * N, (size_t)(n * N), j.copy_threads));
+    const size_t px_bytes = u16 ? sizeof(uint16_t) : sizeof(float);
+    const void* src_img = j.images16 ? (const void*)(j.images16 + lo * N)
+                                     : (u16 ? (const void*)s.h_in16 : (const void*)(j.images + lo * N));
     const float* src_init = j.inits ? j.inits + lo * P : nullptr;  // NULL: the fit kernel estimates them
     if (!j.pinned_in) {
-      par_memcpy(s.h_in, src_img, n * N * px_bytes, j.copy_threads);
-      if (src_init) std::memcpy(s.h_in + s.cap_spots * N, src_init, n * P * sizeof(float));
-      src_img = s.h_in;
-      if (src_init) src_init = s.h_in + s.cap_spots * N;
+      if (!(u16 && !j.images16)) {  // a narrowed chunk is already in pinned memory
+        par_memcpy(s.h_in, src_img, n * N * px_bytes, j.copy_threads);
+        src_img = s.h_in;
+      }
+      if (src_init) {
+        std::memcpy(s.h_in + s.cap_spots * N, src_init, n * P * sizeof(float));
+        src_init = s.h_in + s.cap_spots * N;
+      }
     }
     // inits first, then pixels: the fit needs nothing else, so it can start (and fill the previous
     // fit's tail) as soon as the copy engine is done.  (A widening kernel between the two copies
     // made the init copy wait behind the next chunks' pixel copies: tools/e2e_trace.py.)
     if (src_init)
       SF_CUDA(cudaMemcpyAsync(s.d_init, src_init, n * P * sizeof(float), cudaMemcpyHostToDevice, s.stream));
-    if (j.images16) {
+    if (u16) {
       SF_CUDA(cudaMemcpyAsync(s.d_img16, src_img, n * N * px_bytes, cudaMemcpyHostToDevice, s.stream));
       SF_CUDA(mark(s.stream));
     } else {
@@ -479,14 +501,14 @@ int run_shard(int dev, HostJob& j) {
     SF_CUDA(mark(s.stream));
     sf::LaunchFit a;
     a.images = s.d_img;
-    a.images16 = j.images16 ? s.d_img16 : nullptr;  // staged as u16 by the fit kernel itself
+    a.images16 = u16 ? s.d_img16 : nullptr;  // staged as u16 by the fit kernel itself
     a.inits = s.d_init;
     if (!j.inits) {  // no inits: estimate them on the device from the chunk just copied
       if (n <= sf::kFusedInitMaxSpots) {
         a.inits = nullptr;  // the fit kernel's fused initializer
       } else {
         // P = 5: (x, y, sigma, alpha, beta), as batch_engine._auto_inits builds it
-        const cudaError_t e = j.images16 ? sf::launch_estimate_initial_u16(s.d_img16, j.W, j.H, n, P, kc.lo[2],
+        const cudaError_t e = u16 ? sf::launch_estimate_initial_u16(s.d_img16, j.W, j.H, n, P, kc.lo[2],
                                                                            kc.hi[2], s.d_init, nullptr, s.stream)
                                          : sf::launch_estimate_initial(s.d_img, j.W, j.H, n, P, kc.lo[2], kc.hi[2],
                                                                        s.d_init, nullptr, s.stream);
@@ -885,7 +907,7 @@ static int fit_batch_impl(const float* images, const uint16_t* images16, int32_t
     SF_CUDA(guard.set(dptr_dev));
     DevCtx* c = ctx_for(dptr_dev);
     std::lock_guard<std::mutex> lk(c->mu);
-    if (ensure_ctx(*c, dptr_dev, 1, width * height, cfg->model, false) != 0) return -1;
+    if (ensure_ctx(*c, dptr_dev, 1, width * height, cfg->model, false, false) != 0) return -1;
     cudaStream_t st = c->slot[0].stream;
     SF_CUDA(cudaMemsetAsync(c->d_evals, 0, 3 * sizeof(unsigned long long), st));
     SF_CUDA(cudaEventRecord(c->slot[0].ev[1], st));

@@ -1,0 +1,96 @@
+// sf_host_narrow.cpp -- lossless f32 -> u16 narrowing of host spot chunks for the PCIe leg.
+//
+// The host pipeline (sf_capi.cu:run_shard) is bound by the H2D copy of the pixels (PCIe Gen5 x16,
+// ~53 GB/s: 5.9e7 15x15 f32 fits/s).  Camera counts -- and every image the reference simulator
+// emits ("non-negative integers representable exactly in 32-bit reals") -- are integers
+// in [0, 65535], which 16 bits hold exactly.  For such a chunk the CPU writes the u16 values into a
+// pinned buffer, half the bytes cross PCIe, and the fit kernel widens them back exactly
+// (fit_kernel<..., uint16_t>, bitwise the same fit: tests/test_gpu_parity.py u16 tests).  A chunk with
+// any other value (fraction, negative, -0.0, > 65535, inf, NaN) is sent as f32 unchanged, so results
+// never depend on the narrowing.  AVX2 when the CPU has it (runtime check), scalar otherwise, split
+// over threads.
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <thread>
+#include <vector>
+
+#include <immintrin.h>
+
+#include "spotfit.h"
+
+namespace {
+
+// exactly representable as u16 with the same float value and a clear sign bit
+inline bool narrow_one(float v, uint16_t& out) {
+  uint32_t b;
+  memcpy(&b, &v, 4);
+  if (b > 0x477FFF00u) return false;  // sign set (incl. -0.0), > 65535.0f, inf, NaN
+  const uint32_t u = (uint32_t)v;     // v in [0, 65535]: truncation is exact for integers
+  out = (uint16_t)u;
+  return (float)u == v;
+}
+
+bool narrow_scalar(uint16_t* dst, const float* src, size_t n) {
+  bool ok = true;
+  for (size_t i = 0; i < n; ++i) ok &= narrow_one(src[i], dst[i]);
+  return ok;
+}
+
+__attribute__((target("avx2"))) bool narrow_avx2(uint16_t* dst, const float* src, size_t n) {
+  const __m256i lim = _mm256_set1_epi32(0x477FFF00);
+  __m256i bad = _mm256_setzero_si256();
+  size_t i = 0;
+  for (; i + 16 <= n; i += 16) {
+    const __m256 v0 = _mm256_loadu_ps(src + i), v1 = _mm256_loadu_ps(src + i + 8);
+    const __m256i b0 = _mm256_castps_si256(v0), b1 = _mm256_castps_si256(v1);
+    // signed compare: sign-set patterns are negative (> lim fails, < 0 caught by the gt below)
+    const __m256i r0 = _mm256_or_si256(_mm256_cmpgt_epi32(b0, lim), _mm256_cmpgt_epi32(_mm256_setzero_si256(), b0));
+    const __m256i r1 = _mm256_or_si256(_mm256_cmpgt_epi32(b1, lim), _mm256_cmpgt_epi32(_mm256_setzero_si256(), b1));
+    const __m256i i0 = _mm256_cvttps_epi32(v0), i1 = _mm256_cvttps_epi32(v1);
+    const __m256 e0 = _mm256_cmp_ps(_mm256_cvtepi32_ps(i0), v0, _CMP_NEQ_UQ);  // fraction (or NaN)
+    const __m256 e1 = _mm256_cmp_ps(_mm256_cvtepi32_ps(i1), v1, _CMP_NEQ_UQ);
+    bad = _mm256_or_si256(bad, _mm256_or_si256(_mm256_or_si256(r0, r1),
+                                               _mm256_or_si256(_mm256_castps_si256(e0), _mm256_castps_si256(e1))));
+    // pack to u16 (per 128-bit lane), then restore element order
+    const __m256i p = _mm256_permute4x64_epi64(_mm256_packus_epi32(i0, i1), 0xD8);
+    _mm256_storeu_si256(reinterpret_cast<__m256i*>(dst + i), p);
+  }
+  bool ok = _mm256_testz_si256(bad, bad) != 0;
+  for (; i < n; ++i) ok &= narrow_one(src[i], dst[i]);
+  return ok;
+}
+
+bool narrow_block(uint16_t* dst, const float* src, size_t n) {
+  static const bool avx2 = __builtin_cpu_supports("avx2");
+  return avx2 ? narrow_avx2(dst, src, n) : narrow_scalar(dst, src, n);
+}
+
+}  // namespace
+
+namespace sf {
+
+// dst[i] = (uint16_t)src[i] for i < n over `threads` threads; true iff every value narrowed exactly
+bool par_narrow_u16(uint16_t* dst, const float* src, size_t n, int threads) {
+  constexpr size_t kPiece = 1u << 20;  // elements
+  const int T = (int)std::min<size_t>((size_t)std::max(1, threads), (n + kPiece - 1) / kPiece);
+  if (T <= 1) return narrow_block(dst, src, n);
+  const size_t per = ((n + T - 1) / T + 15) & ~(size_t)15;
+  std::vector<char> ok(T, 1);
+  std::vector<std::thread> th;
+  for (int t = 1; t < T; ++t) {
+    const size_t a = std::min(n, per * t), b = std::min(n, per * (t + 1));
+    th.emplace_back([&, t, a, b] { ok[t] = narrow_block(dst + a, src + a, b - a); });
+  }
+  ok[0] = narrow_block(dst, src, std::min(n, per));
+  for (auto& x : th) x.join();
+  return std::all_of(ok.begin(), ok.end(), [](char c) { return c != 0; });
+}
+
+}  // namespace sf
+
+extern "C" int sf_debug_narrow_u16(const float* src, int64_t n, uint16_t* dst, int32_t threads) {
+  if (n < 0 || (n > 0 && (!src || !dst))) return -1;
+  return sf::par_narrow_u16(dst, src, (size_t)n, threads) ? 1 : 0;
+}

@@ -79,6 +79,10 @@ cudaError_t launch_model_chi_gradient(const float* g, const float* f, const floa
                                       const float* beta, const double* dalpha, const double* dbeta, int N, int P,
                                       int64_t count, double* grad, float* dmat, cudaStream_t st);
 
+// lossless f32 -> u16 narrowing of a host chunk for the PCIe leg (sf_host_narrow.cpp): true iff every
+// value is an integer in [0, 65535] with a clear sign bit
+bool par_narrow_u16(uint16_t* dst, const float* src, size_t n, int threads);
+
 // device simulator (sf_sim.cu)
 cudaError_t launch_simulate(const sf_sim_config& c, int W, int H, int64_t first, int64_t count, float* images,
                             float* truth, cudaStream_t stream);
