@@ -29,7 +29,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off",
                      "-Xptxas", "-v", f"-I{INCLUDE}", f"-I{CSRC}"]
 UNITS = [(p, s) for p in (3, 4, 5) for s in (1, 2, 4, 8, 16)]
-HEADERS = ["sf_device.cuh", "sf_fit_kernel.cuh", "sf_init_core.cuh", "sf_launch.h", "sf_geometry.h", "sf_sim_core.h"]
+HEADERS = ["sf_device.cuh", "sf_fit_kernel.cuh", "sf_fit2l.cuh", "sf_init_core.cuh", "sf_launch.h", "sf_geometry.h", "sf_sim_core.h"]
 
 
 def nvcc() -> str:

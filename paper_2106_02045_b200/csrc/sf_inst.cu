@@ -3,6 +3,11 @@
 // Chain / tail pixel counts are uniform runtime loop bounds (Geom::ch, tl), so
 // one kernel per (P, SLOTS) serves every grid with that pairwise-tree depth.
 #include "sf_launch.h"
+#if SF_P == 3 && SF_SLOTS == 2
+#include <cstdlib>
+
+#include "sf_fit2l.cuh"
+#endif
 
 #ifndef SF_P
 #error "compile with -DSF_P=3|4 -DSF_SLOTS=1|2|4|8|16"
@@ -13,8 +18,48 @@
 
 namespace sf {
 
+#if SF_P == 3 && SF_SLOTS == 2
+// Two-leaf spots with float pixels and given inits: the two-leaves-per-lane kernel with its
+// profile cache in Tensor Memory (sf_fit2l.cuh).  SPOTFIT_FIT2L=0 selects the general kernel.
+static int launch_fit2l(const LaunchFit& a, cudaError_t* err) {
+  auto kern = a.geom.full ? fit_kernel2l<true> : fit_kernel2l<false>;
+  const size_t smem = l2::Smem::bytes(a.geom.ch, a.geom.tl, a.geom.N);
+  *err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (*err != cudaSuccess) return 0;
+  *err = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (*err != cudaSuccess) return 0;
+  int per_sm = 0;
+  *err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, l2::TPB, smem);
+  if (*err != cudaSuccess) return 0;
+  // TMEM: 512 columns per SM.  The occupancy API reports 1 CTA per SM for this kernel (it uses
+  // tcgen05); registers (128 x 128 threads), shared memory (< 57 KB) and TMEM (128 columns) all allow 4.
+  (void)per_sm;
+  per_sm = 512 / l2::kCols;
+  int64_t blocks = (int64_t)per_sm * a.sm_count;
+  const int64_t need = (a.count + l2::GPB - 1) / l2::GPB;
+  if (blocks > need) blocks = need;
+  if (blocks < 1) return 0;
+  kern<<<(unsigned)blocks, l2::TPB, smem, a.stream>>>(a.images, a.inits, a.count, a.geom, a.cfg, a.out);
+  *err = cudaGetLastError();
+  return (int)blocks;
+}
+
+static bool use_fit2l(const LaunchFit& a) {
+  static const bool on = [] {
+    const char* e = std::getenv("SPOTFIT_FIT2L");
+    return !(e && e[0] == '0');
+  }();
+  return on && a.inits != nullptr && a.images16 == nullptr && a.geom.ch <= 2 * l2::kMaxPairs + 1;
+}
+#endif
+
 template <typename PX>
 static int launch_fit_px(const LaunchFit& a, const PX* images, cudaError_t* err) {
+#if SF_P == 3 && SF_SLOTS == 2
+  if constexpr (sizeof(PX) == 4) {
+    if (use_fit2l(a)) return launch_fit2l(a, err);
+  }
+#endif
   const bool fused = a.inits == nullptr;
   auto kern = a.geom.full ? (fused ? fit_kernel<SF_P, SF_SLOTS, true, PX, true> : fit_kernel<SF_P, SF_SLOTS, true, PX, false>)
                           : (fused ? fit_kernel<SF_P, SF_SLOTS, false, PX, true> : fit_kernel<SF_P, SF_SLOTS, false, PX, false>);

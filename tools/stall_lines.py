@@ -21,7 +21,7 @@ for r in data:
     off=int(r[ia],16)-base; s=int(r[iss] or 0); e=int(r[iex] or 0)
     k=amap.get(off,('?',0)); by[k][0]+=s; by[k][1]+=e; tot+=s; totx+=e
 print("mismatch",mism,"total samples",tot,"inst",totx)
-src={f:open("/root/repo/paper_2106_02045_b200/csrc/"+f).read().splitlines() for f in ("sf_device.cuh","sf_fit_kernel.cuh","sf_init_core.cuh","sf_init.cu")}
+src={f:open("/root/repo/paper_2106_02045_b200/csrc/"+f).read().splitlines() for f in ("sf_device.cuh","sf_fit_kernel.cuh","sf_init_core.cuh","sf_init.cu","sf_fit2l.cuh")}
 for k,(s,e) in sorted(by.items(), key=lambda x:-x[1][0])[:int(sys.argv[3]) if len(sys.argv)>3 else 40]:
     t=src.get(k[0],[''])[k[1]-1].strip()[:70] if k[0] in src and k[1]>0 else ''
     print(f"{k[0][:14]:14s}:{k[1]:5d} {100*s/tot:5.1f}% samp {100*e/totx:5.1f}% inst  {t}")
