@@ -110,6 +110,7 @@ struct Lane {
   uint32_t own[2];  // per virtual lane: bit j chain slot j < ch, bit ch + t tail t
   int base[2], tbase[2];
   int ch, tl;
+  int tlv[2];       // tail pixels of each leaf (a leaf without tail skips its zero tail terms)
   uint32_t tw;      // TMEM address of this warp's lane quarter, column 0
 };
 
@@ -270,14 +271,15 @@ __device__ __forceinline__ void evaluate2l(Smem& S, const Lane& L, double G, dou
     else
       chain1_2l<FULL, false>(S, L, v, pe, ix, nz2, a1);
     const uint32_t own = v ? L.own[1] : L.own[0];
+    const int tlv = v ? L.tlv[1] : L.tlv[0];  // (+0.0 terms of unowned tail slots leave the sums unchanged)
 #pragma unroll 1
-    for (int t = 0; t < L.tl; ++t) {  // tail profiles (added after the 8-way combine)
+    for (int t = 0; t < tlv; ++t) {  // tail profiles (added after the 8-way combine)
       const int r = v * S.ns + so0 + t;
       float f, fg[3];
       pixel_profile<3>(S.sxy[(so0 + t) * 16 + 8 * v + L.gl], pe, ix, ix, owns(own, L.ch + t), f, fg);
       S.sfq[r * TPB + tid] = make_float4(f, fg[0], fg[1], fg[2]);
     }
-    combine_leaf<12>(a1, pk, res, tbuf, v, L.tl, [&](int t, float (&tt)[12]) {
+    combine_leaf<12>(a1, pk, res, tbuf, v, tlv, [&](int t, float (&tt)[12]) {
       const int r = v * S.ns + so0 + t;
       const float4 q = S.sfq[r * TPB + tid];
       const float fg[3] = {q.y, q.z, q.w};
@@ -337,7 +339,8 @@ __device__ __forceinline__ void evaluate2l(Smem& S, const Lane& L, double G, dou
     else
       chain2_2l<FULL, false>(S, L, v, a32, b32, da, db, nz2, a2);
     const uint32_t own = v ? L.own[1] : L.own[0];
-    combine_leaf<10>(a2, pk, res, tbuf, v, L.tl, [&](int t, float (&tt)[10]) {
+    const int tlv = v ? L.tlv[1] : L.tlv[0];
+    combine_leaf<10>(a2, pk, res, tbuf, v, tlv, [&](int t, float (&tt)[10]) {
       const int r = v * S.ns + so0 + t;
       const float4 q = S.sfq[r * TPB + tid];
       const float fg[3] = {q.y, q.z, q.w};
@@ -451,6 +454,8 @@ __global__ void __launch_bounds__(l2::TPB, 4)
   L.gib = warp * 4 + L.gw;
   L.ch = geom.ch;
   L.tl = geom.tl;
+  L.tlv[0] = geom.nt[0];
+  L.tlv[1] = geom.nt[8];
   L.tw = tmem_base + ((uint32_t)(warp * 32) << 16);
 #pragma unroll
   for (int v = 0; v < 2; ++v) {
