@@ -356,8 +356,8 @@ __device__ __forceinline__ void evaluate2l(Smem& S, const Lane& L, double G, dou
 
 // Scatter the staged spot into both virtual lanes' pixel slots and sum G in numpy order
 // (sf_device.cuh:load_spot for a two-leaf group); tameness flags as load_spot.
-template <bool FULL>
-__device__ __forceinline__ double load_spot2l(Smem& S, const Lane& L, const float* st, bool load, bool& gt, bool& g40) {
+template <bool FULL, typename PX>
+__device__ __forceinline__ double load_spot2l(Smem& S, const Lane& L, const PX* st, bool load, bool& gt, bool& g40) {
   const int tid = threadIdx.x;
   unsigned mx = 0u;
   double sum0 = 0.0, sum1 = 0.0;
@@ -368,7 +368,7 @@ __device__ __forceinline__ double load_spot2l(Smem& S, const Lane& L, const floa
     const int base = v ? L.base[1] : L.base[0], tbase = v ? L.tbase[1] : L.tbase[0];
     auto take = [&](int j, int idx) {
       const bool o = (FULL && j < L.ch) ? true : owns(own, j);
-      const float g = (load && o) ? st[idx] : 0.0f;
+      const float g = (load && o) ? (float)st[idx] : 0.0f;  // u16 counts widen exactly
       mx = max(mx, __float_as_uint(g));
       a[0] = __dadd_rn(a[0], (double)g);
       return g;
@@ -399,8 +399,10 @@ __device__ __forceinline__ double load_spot2l(Smem& S, const Lane& L, const floa
   return __dadd_rn(0.0, __dadd_rn(sum0, sum1));
 }
 
-// The group's 8 lanes stream the 16-B aligned window around the next spot (stage_spot for 8 lanes).
-__device__ __forceinline__ int stage2l(const Smem& S, int gib, int gl, const float* src, uintptr_t lo, uintptr_t hi,
+// The group's 8 lanes stream the 16-B aligned window around the next spot (stage_spot for 8 lanes;
+// PX = float or 16-bit counts).
+template <typename PX>
+__device__ __forceinline__ int stage2l(const Smem& S, int gib, int gl, const PX* src, uintptr_t lo, uintptr_t hi,
                                        int N) {
   const uintptr_t a0 = (uintptr_t)src & ~(uintptr_t)15;
   const uintptr_t e0 = ((uintptr_t)(src + N) + 15) & ~(uintptr_t)15;
@@ -413,23 +415,29 @@ __device__ __forceinline__ int stage2l(const Smem& S, int gib, int gl, const flo
       const uintptr_t cs = a0 + 16 * (uintptr_t)c;
       if (cs >= lo && cs + 16 <= hi) {
         cp_async16(dst + 4 * c, reinterpret_cast<const void*>(cs));
-      } else {
+      } else if constexpr (sizeof(PX) == 4) {
 #pragma unroll
         for (int w = 0; w < 4; ++w)
           if (cs + 4 * w >= lo && cs + 4 * w + 4 <= hi) cp_async4(dst + 4 * c + w, reinterpret_cast<const float*>(cs + 4 * w));
+      } else {  // 2-byte pixels: plain loads (visible to the group after the refill's __syncwarp)
+        PX* d = reinterpret_cast<PX*>(dst + 4 * c);
+#pragma unroll
+        for (int w = 0; w < 16 / (int)sizeof(PX); ++w)
+          if (cs + sizeof(PX) * w >= lo && cs + sizeof(PX) * (w + 1) <= hi)
+            d[w] = *reinterpret_cast<const PX*>(cs + sizeof(PX) * w);
       }
     }
   }
-  return (int)(((uintptr_t)src & 15) / sizeof(float));
+  return (int)(((uintptr_t)src & 15) / sizeof(PX));
 }
 
 }  // namespace l2
 
 // The kernel: fit_kernel's loop (refill -> fused evaluation -> LM step) for two-leaf spots with
-// float pixels and given inits.
-template <bool FULL>
+// given inits; PX: float pixels or 16-bit counts (staged as u16, widened exactly in load_spot2l).
+template <bool FULL, typename PX = float>
 __global__ void __launch_bounds__(l2::TPB, 4)
-    fit_kernel2l(const float* __restrict__ images, const float* __restrict__ inits, int64_t count, const Geom geom,
+    fit_kernel2l(const PX* __restrict__ images, const float* __restrict__ inits, int64_t count, const Geom geom,
                  const Cfg cfg, FitOut out) {
   using namespace l2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -515,7 +523,7 @@ __global__ void __launch_bounds__(l2::TPB, 4)
   };
   auto prefetch = [&](int64_t sp) {
     if (sp < count) {
-      nsh = stage2l(S, L.gib, L.gl, images + sp * (int64_t)N, lo, hi, N);
+      nsh = stage2l<PX>(S, L.gib, L.gl, images + sp * (int64_t)N, lo, hi, N);
 #pragma unroll
       for (int k = 0; k < 3; ++k) nxt[k] = __ldg(inits + sp * 3 + k);
     }
@@ -535,9 +543,9 @@ __global__ void __launch_bounds__(l2::TPB, 4)
       const bool load = need && !exhausted;
       if (load) cp_async_wait_all();
       __syncwarp(kFull);
-      const float* win = S.stage + L.gib * S.sw + nsh;
+      const PX* win = reinterpret_cast<const PX*>(S.stage + L.gib * S.sw) + nsh;
       bool sgt, sg40;
-      const double gsum = load_spot2l<FULL>(S, L, win, load, sgt, sg40);
+      const double gsum = load_spot2l<FULL, PX>(S, L, win, load, sgt, sg40);
       bool bad = false;
       if (load) {
         float init[3];

@@ -19,10 +19,11 @@
 namespace sf {
 
 #if SF_P == 3 && SF_SLOTS == 2
-// Two-leaf spots with float pixels and given inits: the two-leaves-per-lane kernel with its
+// Two-leaf spots with given inits (float or 16-bit pixels): the two-leaves-per-lane kernel with its
 // profile cache in Tensor Memory (sf_fit2l.cuh).  SPOTFIT_FIT2L=0 selects the general kernel.
-static int launch_fit2l(const LaunchFit& a, cudaError_t* err) {
-  auto kern = a.geom.full ? fit_kernel2l<true> : fit_kernel2l<false>;
+template <typename PX>
+static int launch_fit2l(const LaunchFit& a, const PX* images, cudaError_t* err) {
+  auto kern = a.geom.full ? fit_kernel2l<true, PX> : fit_kernel2l<false, PX>;
   const size_t smem = l2::Smem::bytes(a.geom.ch, a.geom.tl, a.geom.N);
   *err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (*err != cudaSuccess) return 0;
@@ -39,7 +40,7 @@ static int launch_fit2l(const LaunchFit& a, cudaError_t* err) {
   const int64_t need = (a.count + l2::GPB - 1) / l2::GPB;
   if (blocks > need) blocks = need;
   if (blocks < 1) return 0;
-  kern<<<(unsigned)blocks, l2::TPB, smem, a.stream>>>(a.images, a.inits, a.count, a.geom, a.cfg, a.out);
+  kern<<<(unsigned)blocks, l2::TPB, smem, a.stream>>>(images, a.inits, a.count, a.geom, a.cfg, a.out);
   *err = cudaGetLastError();
   return (int)blocks;
 }
@@ -49,16 +50,14 @@ static bool use_fit2l(const LaunchFit& a) {
     const char* e = std::getenv("SPOTFIT_FIT2L");
     return !(e && e[0] == '0');
   }();
-  return on && a.inits != nullptr && a.images16 == nullptr && a.geom.ch <= 2 * l2::kMaxPairs + 1;
+  return on && a.inits != nullptr && a.geom.ch <= 2 * l2::kMaxPairs + 1;
 }
 #endif
 
 template <typename PX>
 static int launch_fit_px(const LaunchFit& a, const PX* images, cudaError_t* err) {
 #if SF_P == 3 && SF_SLOTS == 2
-  if constexpr (sizeof(PX) == 4) {
-    if (use_fit2l(a)) return launch_fit2l(a, err);
-  }
+  if (use_fit2l(a)) return launch_fit2l<PX>(a, images, err);
 #endif
   const bool fused = a.inits == nullptr;
   auto kern = a.geom.full ? (fused ? fit_kernel<SF_P, SF_SLOTS, true, PX, true> : fit_kernel<SF_P, SF_SLOTS, true, PX, false>)
