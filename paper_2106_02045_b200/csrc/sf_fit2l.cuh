@@ -1,5 +1,7 @@
-// sf_fit2l.cuh -- the two-leaf fit kernel: spots whose numpy summation tree has exactly two
-// leaves (129..256 pixels, the 15x15 headline), with the per-pixel profile cache in Tensor Memory.
+// sf_fit2l.cuh -- the two-leaves-per-lane fit kernel for symmetric spots of 129..1024 pixels (2, 4
+// or 8 leaves: SL), with the per-pixel profile cache in Tensor Memory.  The text below describes the
+// two-leaf case (the 15x15 headline); with SL leaves a spot takes 4 SL lanes (one octet of lanes per
+// pair of leaves), and the octets' pair sums are combined in numpy's slot-tree order by shuffles.
 //
 // The general kernel (sf_fit_kernel.cuh) gives each chain of the tree its own lane, so a two-leaf
 // spot takes 16 lanes and a warp fits two spots; every warp-level step that is not a pixel loop
@@ -24,24 +26,32 @@ namespace sf {
 namespace l2 {
 
 constexpr int TPB = 128;   // 4 warps
-constexpr int GPB = 16;    // groups (spots) per CTA: 4 per warp, 8 lanes each
+// SL leaves per spot: 4 SL lanes per group, 8 / SL groups per warp, 32 / SL per CTA
+template <int SL>
+__host__ __device__ constexpr int lanes_per_group() { return 4 * SL; }
+template <int SL>
+__host__ __device__ constexpr int groups_per_cta() { return 4 * (8 / SL); }
 constexpr int kCols = 128; // TMEM columns per CTA
 constexpr int kTS = 34;    // scratch row stride in doubles (32 lanes + a 2-double bank skew)
 constexpr int kQA = 12;    // parked leaf-0 rows (pass 1: 12 quantities; pass 2: 10)
 constexpr int kSysQ = 10;  // saved normal system: JtJ (6) + rhs (3), padded
 constexpr int kMaxPairs = 8;
 
+template <int SL>
 struct Smem {
+  static constexpr int GPB = groups_per_cta<SL>();
+  static constexpr int VL = 8 * SL;              // virtual lanes (coordinate table width)
+  static constexpr bool kGen = SL >= 8;          // coordinates generated in registers (no table)
   double* sys;   // [GPB][kSysQ]
   double* kc;    // [2]: ddiv_rcp(lam_down), ddiv_rcp(N - 5)
   double* park;  // [4 warps][kQA][kTS]: one leaf's chain sums
   double* res;   // [4 warps][2][4 groups][kQA]: leaf-0 sums, then the group sums
   float* tbuf;   // [4 warps][4 groups][kQA]: tail terms of one tail slot
   float2* g;     // [2][np][TPB]: pixel values of chain slot pairs (0 where not owned)
-  float4* xy;    // [np][16]: pair coordinates (x_A, x_B, y_A, y_B) per virtual lane
+  float4* xy;    // [np][VL]: pair coordinates (x_A, x_B, y_A, y_B) per virtual lane (not when kGen)
   float4* sfq;   // [2][ns][TPB]: solo slots (odd last chain slot, tails): f, df/dx, df/dy, df/ds
   float* sg;     // [2][ns][TPB]: solo pixel values
-  float2* sxy;   // [ns][16]: solo coordinates
+  float2* sxy;   // [ns][VL]: solo coordinates (not when kGen)
   float* stage;  // [GPB][sw]: next-spot staging windows
   int np, ns, sw;
 
@@ -51,7 +61,8 @@ struct Smem {
     return (size_t)GPB * kSysQ * 8 + 16 + (size_t)4 * kQA * kTS * 8 + (size_t)4 * 2 * 4 * kQA * 8 +
            (size_t)4 * 4 * kQA * 4 +
            (size_t)2 * np * TPB * 8 +
-           (size_t)np * 16 * 16 + (size_t)2 * ns * TPB * 16 + (size_t)2 * ns * TPB * 4 + (size_t)ns * 16 * 8 +
+           (kGen ? 0 : (size_t)np * VL * 16) + (size_t)2 * ns * TPB * 16 + (size_t)2 * ns * TPB * 4 +
+           (kGen ? 0 : (size_t)ns * VL * 8) +
            (size_t)GPB * stage_floats(N) * 4 + 64;
   }
   __device__ __forceinline__ void bind(unsigned char* raw, int ch, int tl, int N) {
@@ -72,13 +83,13 @@ struct Smem {
     g = reinterpret_cast<float2*>(p);
     p += (size_t)2 * np * TPB * 8;
     xy = reinterpret_cast<float4*>(p);
-    p += (size_t)np * 16 * 16;
+    p += kGen ? 0 : (size_t)np * VL * 16;
     sfq = reinterpret_cast<float4*>(p);
     p += (size_t)2 * ns * TPB * 16;
     sg = reinterpret_cast<float*>(p);
     p += (size_t)2 * ns * TPB * 4;
     sxy = reinterpret_cast<float2*>(p);
-    p += (size_t)ns * 16 * 8;
+    p += kGen ? 0 : (size_t)ns * VL * 8;
     stage = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(p) + 15) & ~(uintptr_t)15);
   }
 };
@@ -107,6 +118,8 @@ __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sy
 // One thread's view: lane in group, its two virtual lanes' ownership and pixel bases.
 struct Lane {
   int gl, gw, gib;  // lane in group, group in warp, group in CTA
+  int vl0;          // virtual lane of leaf 0 (leaf 1: vl0 + 8): 16 * octet + chain
+  float basef[2], tbasef[2], Wf, invW;  // coordinate generation (SL >= 8)
   uint32_t own[2];  // per virtual lane: bit j chain slot j < ch, bit ch + t tail t
   int base[2], tbase[2];
   int ch, tl;
@@ -115,34 +128,62 @@ struct Lane {
 };
 
 // ---------------------------------------------------------------------------------- pass loops
+// Coordinates of chain slot pair i (slots 2i, 2i+1) of virtual lane vl: the table, or generated
+// in registers when SL >= 8 (sf_device.cuh:pair_xy: y = floor((idx + 0.5) / W) by the RNE magic number).
+template <int SL>
+__device__ __forceinline__ void pair_xy2l(const float4* xyp, const Lane& L, int v, int i, f2 nz, f2& cx, f2& cy) {
+  if constexpr (Smem<SL>::kGen) {
+    const float iA = __fmaf_rn(16.0f, (float)i, v ? L.basef[1] : L.basef[0]);
+    const f2 idx = pk2(iA, __fadd_rn(iA, 8.0f));
+    const f2 t = mul2(add2(idx, bc2(0.5f)), bc2(L.invW), nz);
+    cy = sub2(add2(sub2(t, bc2(0.5f)), bc2(12582912.0f)), bc2(12582912.0f));
+    cx = fma2(bc2(-L.Wf), cy, idx);
+  } else {  // xyp: this virtual lane's table entry of pair i
+    const float4 c = *xyp;
+    cx = pk2(c.x, c.y);
+    cy = pk2(c.z, c.w);
+  }
+}
+// Coordinates of solo slot j (j >= ch & ~1: the odd last chain slot or tail j - ch) of virtual lane vl.
+template <int SL>
+__device__ __forceinline__ float2 solo_xy2l(const Smem<SL>& S, const Lane& L, int v, int vl, int j) {
+  if constexpr (Smem<SL>::kGen) {
+    const float idx = j < L.ch ? __fmaf_rn(8.0f, (float)j, v ? L.basef[1] : L.basef[0])
+                               : __fadd_rn(v ? L.tbasef[1] : L.tbasef[0], (float)(j - L.ch));
+    const float t = __fmul_rn(__fadd_rn(idx, 0.5f), L.invW);
+    const float y = __fsub_rn(__fadd_rn(__fsub_rn(t, 0.5f), 12582912.0f), 12582912.0f);
+    return make_float2(__fmaf_rn(-L.Wf, y, idx), y);
+  } else {
+    return S.sxy[(j - (L.ch & ~1)) * Smem<SL>::VL + vl];
+  }
+}
+
 // Pass-1 chain loop of virtual lane v (leaf v): pair loop (profiles to TMEM), odd last slot.
-template <bool FULL, bool GT>
-__device__ __forceinline__ void chain1_2l(Smem& S, const Lane& L, int v, const float (&pe)[3], float ix,
+template <int SL, bool FULL, bool GT>
+__device__ __forceinline__ void chain1_2l(Smem<SL>& S, const Lane& L, int v, const float (&pe)[3], float ix,
                                           unsigned long long nz2, double (&a1)[12]) {
   const f2 nz{nz2};
   const f2 x0 = bc2(pe[0]), y0 = bc2(pe[1]), ix2 = bc2(ix);
-  const int tid = threadIdx.x, vl = 8 * v + L.gl;
+  const int tid = threadIdx.x, vl = L.vl0 + 8 * v;
   const uint32_t own = v ? L.own[1] : L.own[0];
 #pragma unroll
   for (int q = 0; q < 12; ++q) a1[q] = 0.0;
-  const float4* xyp = S.xy + vl;                  // pair i: xyp[16 i]
   const float2* gp = S.g + v * S.np * TPB + tid;  // pair i: gp[TPB i]
+  const float4* xyp = S.xy + vl;                  // pair i: xyp[VL i] (coordinate table)
   uint32_t tc = L.tw + (uint32_t)(v * S.np * 8);  // pair i: column tc + 8 i
 #pragma unroll 1
-  for (int i = 0; i < S.np; ++i, xyp += 16, gp += TPB, tc += 8) {
-    const float4 c = *xyp;
-    f2 f, fg[3], t[12];
-    pixel_profile2<3, FULL>(pk2(c.x, c.y), pk2(c.z, c.w), x0, y0, ix2, ix2, nz, owns(own, 2 * i),
-                            owns(own, 2 * i + 1), f, fg);
+  for (int i = 0; i < S.np; ++i, gp += TPB, tc += 8, xyp += Smem<SL>::VL) {
+    f2 cx, cy, f, fg[3], t[12];
+    pair_xy2l<SL>(xyp, L, v, i, nz, cx, cy);
+    pixel_profile2<3, FULL>(cx, cy, x0, y0, ix2, ix2, nz, owns(own, 2 * i), owns(own, 2 * i + 1), f, fg);
     tm_st8(tc, f, fg[0], fg[1], fg[2]);
     const float2 g = *gp;
     pass1_terms2<3>(f, fg, pk2(g.x, g.y), nz, t);
     acc_pair2<12, 3, 1, GT>(a1, t);
   }
   if (L.ch & 1) {  // odd chain length: last chain slot, scalar, cached in shared memory
-    const float2 c = S.sxy[vl];
     float f, fg[3], t[12];
-    pixel_profile<3>(c, pe, ix, ix, owns(own, L.ch - 1), f, fg);
+    pixel_profile<3>(solo_xy2l<SL>(S, L, v, vl, L.ch - 1), pe, ix, ix, owns(own, L.ch - 1), f, fg);
     S.sfq[(v * S.ns) * TPB + tid] = make_float4(f, fg[0], fg[1], fg[2]);
     pass1_terms<3>(f, fg, S.sg[(v * S.ns) * TPB + tid], t);
     acc1<12, 3, 1>(a1, t, GT);
@@ -151,8 +192,8 @@ __device__ __forceinline__ void chain1_2l(Smem& S, const Lane& L, int v, const f
 }
 
 // Pass-2 chain loop of virtual lane v (profiles from TMEM).
-template <bool FULL, bool T2>
-__device__ __forceinline__ void chain2_2l(Smem& S, const Lane& L, int v, float a32, float b32, const float (&da)[3],
+template <int SL, bool FULL, bool T2>
+__device__ __forceinline__ void chain2_2l(Smem<SL>& S, const Lane& L, int v, float a32, float b32, const float (&da)[3],
                                           const float (&db)[3], unsigned long long nz2, double (&a2)[10]) {
   const f2 nz{nz2};
   const f2 a2p = bc2(a32), b2p = bc2(b32);
@@ -193,7 +234,7 @@ __device__ __forceinline__ void chain2_2l(Smem& S, const Lane& L, int v, float a
 // quantities l8 and l8 + 8.  Leaf 0 (v = 0) leaves its sums in res; leaf 1 adds them (the depth-1
 // slot tree, leaf 0 + leaf 1), applies numpy's outer 0.0 + and broadcasts the group sums into a[]
 // of every lane of the group.  All 32 lanes of the warp call it.
-template <int Q, class Tail>
+template <int SL, int Q, class Tail>
 __device__ __forceinline__ void combine_leaf(double (&a)[Q], double* pk, double* res, float* tb, int v, int tl,
                                              Tail&& tail) {
   const int lane = threadIdx.x & 31, l8 = lane & 7, g0 = lane & ~7, gw = lane >> 3;
@@ -235,8 +276,10 @@ __device__ __forceinline__ void combine_leaf(double (&a)[Q], double* pk, double*
     if (q < Q) {
       if (v == 0)
         r0[q] = sc[r];
-      else
+      else if (SL == 2)  // the whole tree: leaf 0 + leaf 1, then numpy's outer 0.0 +
         r0[4 * kQA + q] = __dadd_rn(0.0, __dadd_rn(r0[q], sc[r]));
+      else  // this octet's pair of leaves; the slot tree continues across octets below
+        r0[4 * kQA + q] = __dadd_rn(r0[q], sc[r]);
     }
   }
   __syncwarp();
@@ -248,12 +291,20 @@ __device__ __forceinline__ void combine_leaf(double (&a)[Q], double* pk, double*
       a[2 * k] = t.x;
       a[2 * k + 1] = t.y;
     }
+    if constexpr (SL >= 4) {  // slot tree over the group's octets (xor 8, then 16), then 0.0 +
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        a[q] = __dadd_rn(a[q], shfl_xor_d(a[q], 8));
+        if constexpr (SL >= 8) a[q] = __dadd_rn(a[q], shfl_xor_d(a[q], 16));
+        a[q] = __dadd_rn(0.0, a[q]);
+      }
+    }
     __syncwarp();
   }
 }
 
-template <bool FULL>
-__device__ __forceinline__ void evaluate2l(Smem& S, const Lane& L, double G, double n, const float (&pe)[3], bool gt,
+template <int SL, bool FULL>
+__device__ __forceinline__ void evaluate2l(Smem<SL>& S, const Lane& L, double G, double n, const float (&pe)[3], bool gt,
                                            bool lane_g40, bool care, unsigned long long nz2, Eval<3>& E) {
   const int tid = threadIdx.x;
   double* pk = S.park + (size_t)(tid >> 5) * kQA * kTS;
@@ -267,19 +318,19 @@ __device__ __forceinline__ void evaluate2l(Smem& S, const Lane& L, double G, dou
 #pragma unroll 1
   for (int v = 0; v < 2; ++v) {
     if (gt)
-      chain1_2l<FULL, true>(S, L, v, pe, ix, nz2, a1);
+      chain1_2l<SL, FULL, true>(S, L, v, pe, ix, nz2, a1);
     else
-      chain1_2l<FULL, false>(S, L, v, pe, ix, nz2, a1);
+      chain1_2l<SL, FULL, false>(S, L, v, pe, ix, nz2, a1);
     const uint32_t own = v ? L.own[1] : L.own[0];
     const int tlv = v ? L.tlv[1] : L.tlv[0];  // (+0.0 terms of unowned tail slots leave the sums unchanged)
 #pragma unroll 1
     for (int t = 0; t < tlv; ++t) {  // tail profiles (added after the 8-way combine)
       const int r = v * S.ns + so0 + t;
       float f, fg[3];
-      pixel_profile<3>(S.sxy[(so0 + t) * 16 + 8 * v + L.gl], pe, ix, ix, owns(own, L.ch + t), f, fg);
+      pixel_profile<3>(solo_xy2l<SL>(S, L, v, L.vl0 + 8 * v, L.ch + t), pe, ix, ix, owns(own, L.ch + t), f, fg);
       S.sfq[r * TPB + tid] = make_float4(f, fg[0], fg[1], fg[2]);
     }
-    combine_leaf<12>(a1, pk, res, tbuf, v, tlv, [&](int t, float (&tt)[12]) {
+    combine_leaf<SL, 12>(a1, pk, res, tbuf, v, tlv, [&](int t, float (&tt)[12]) {
       const int r = v * S.ns + so0 + t;
       const float4 q = S.sfq[r * TPB + tid];
       const float fg[3] = {q.y, q.z, q.w};
@@ -291,7 +342,7 @@ __device__ __forceinline__ void evaluate2l(Smem& S, const Lane& L, double G, dou
   const double F = a1[0], FF = a1[1], FG = a1[2];
   const double denom = n * FF - F * F;
   E.singular = denom <= 1e-12 * n * FF;
-  const int tb = (tid & 31) & ~7;
+  const int tb = (tid & 31) & ~(lanes_per_group<SL>() - 1);  // the group's lanes share the divisions
   const int k = (tid & 31) - tb;
   const double rden = ddiv_rcp(denom);
   {
@@ -335,12 +386,12 @@ __device__ __forceinline__ void evaluate2l(Smem& S, const Lane& L, double G, dou
 #pragma unroll 1
   for (int v = 0; v < 2; ++v) {
     if (t2)
-      chain2_2l<FULL, true>(S, L, v, a32, b32, da, db, nz2, a2);
+      chain2_2l<SL, FULL, true>(S, L, v, a32, b32, da, db, nz2, a2);
     else
-      chain2_2l<FULL, false>(S, L, v, a32, b32, da, db, nz2, a2);
+      chain2_2l<SL, FULL, false>(S, L, v, a32, b32, da, db, nz2, a2);
     const uint32_t own = v ? L.own[1] : L.own[0];
     const int tlv = v ? L.tlv[1] : L.tlv[0];
-    combine_leaf<10>(a2, pk, res, tbuf, v, tlv, [&](int t, float (&tt)[10]) {
+    combine_leaf<SL, 10>(a2, pk, res, tbuf, v, tlv, [&](int t, float (&tt)[10]) {
       const int r = v * S.ns + so0 + t;
       const float4 q = S.sfq[r * TPB + tid];
       const float fg[3] = {q.y, q.z, q.w};
@@ -356,8 +407,8 @@ __device__ __forceinline__ void evaluate2l(Smem& S, const Lane& L, double G, dou
 
 // Scatter the staged spot into both virtual lanes' pixel slots and sum G in numpy order
 // (sf_device.cuh:load_spot for a two-leaf group); tameness flags as load_spot.
-template <bool FULL, typename PX>
-__device__ __forceinline__ double load_spot2l(Smem& S, const Lane& L, const PX* st, bool load, bool& gt, bool& g40) {
+template <int SL, bool FULL, typename PX>
+__device__ __forceinline__ double load_spot2l(Smem<SL>& S, const Lane& L, const PX* st, bool load, bool& gt, bool& g40) {
   const int tid = threadIdx.x;
   unsigned mx = 0u;
   double sum0 = 0.0, sum1 = 0.0;
@@ -396,22 +447,26 @@ __device__ __forceinline__ double load_spot2l(Smem& S, const Lane& L, const PX* 
   }
   gt = mx < 0x71800000u;
   g40 = mx < 0x53800000u;
-  return __dadd_rn(0.0, __dadd_rn(sum0, sum1));
+  double g = __dadd_rn(sum0, sum1);  // this octet's pair of leaves, then the slot tree over octets
+  if constexpr (SL >= 4) g = __dadd_rn(g, shfl_xor_d(g, 8));
+  if constexpr (SL >= 8) g = __dadd_rn(g, shfl_xor_d(g, 16));
+  return __dadd_rn(0.0, g);
 }
 
 // The group's 8 lanes stream the 16-B aligned window around the next spot (stage_spot for 8 lanes;
 // PX = float or 16-bit counts).
-template <typename PX>
-__device__ __forceinline__ int stage2l(const Smem& S, int gib, int gl, const PX* src, uintptr_t lo, uintptr_t hi,
+template <int SL, typename PX>
+__device__ __forceinline__ int stage2l(const Smem<SL>& S, int gib, int gl, const PX* src, uintptr_t lo, uintptr_t hi,
                                        int N) {
+  constexpr int LG = lanes_per_group<SL>();
   const uintptr_t a0 = (uintptr_t)src & ~(uintptr_t)15;
   const uintptr_t e0 = ((uintptr_t)(src + N) + 15) & ~(uintptr_t)15;
   const int nck = (int)((e0 - a0) >> 4);
   float* dst = S.stage + gib * S.sw;
   if (a0 >= lo && e0 <= hi) {
-    for (int c = gl; c < nck; c += 8) cp_async16(dst + 4 * c, reinterpret_cast<const void*>(a0 + 16 * (uintptr_t)c));
+    for (int c = gl; c < nck; c += LG) cp_async16(dst + 4 * c, reinterpret_cast<const void*>(a0 + 16 * (uintptr_t)c));
   } else {
-    for (int c = gl; c < nck; c += 8) {
+    for (int c = gl; c < nck; c += LG) {
       const uintptr_t cs = a0 + 16 * (uintptr_t)c;
       if (cs >= lo && cs + 16 <= hi) {
         cp_async16(dst + 4 * c, reinterpret_cast<const void*>(cs));
@@ -435,14 +490,15 @@ __device__ __forceinline__ int stage2l(const Smem& S, int gib, int gl, const PX*
 
 // The kernel: fit_kernel's loop (refill -> fused evaluation -> LM step) for two-leaf spots with
 // given inits; PX: float pixels or 16-bit counts (staged as u16, widened exactly in load_spot2l).
-template <bool FULL, typename PX = float>
+template <int SL, bool FULL, typename PX = float>
 __global__ void __launch_bounds__(l2::TPB, 4)
     fit_kernel2l(const PX* __restrict__ images, const float* __restrict__ inits, int64_t count, const Geom geom,
                  const Cfg cfg, FitOut out) {
   using namespace l2;
+  constexpr int LG = lanes_per_group<SL>(), GPW = 32 / LG, VL = l2::Smem<SL>::VL;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ uint32_t tmem_base;
-  l2::Smem S;
+  l2::Smem<SL> S;
   S.bind(smem_raw, geom.ch, geom.tl, geom.N);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // TMEM: 128 columns for the CTA (4 CTAs per SM use all 512)
@@ -456,21 +512,32 @@ __global__ void __launch_bounds__(l2::TPB, 4)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n");
 
+  // lane -> group (LG lanes), octet of the group (a pair of leaves), chain k of both leaves
   l2::Lane L;
-  L.gl = lane & 7;
-  L.gw = lane >> 3;
-  L.gib = warp * 4 + L.gw;
+  L.gl = lane & (LG - 1);
+  L.gw = lane / LG;
+  L.gib = warp * GPW + L.gw;
+  L.vl0 = 16 * (L.gl >> 3) + (lane & 7);
   L.ch = geom.ch;
   L.tl = geom.tl;
-  L.tlv[0] = geom.nt[0];
-  L.tlv[1] = geom.nt[8];
-  L.tw = tmem_base + ((uint32_t)(warp * 32) << 16);
+  // tail loop bound per leaf slot, uniform over the warp's octets (their leaves' largest tail)
 #pragma unroll
   for (int v = 0; v < 2; ++v) {
-    const int vl = 8 * v + L.gl;
+    int m = 0;
+    for (int o = 0; o < SL / 2; ++o) m = max(m, (int)geom.nt[16 * o + 8 * v]);
+    L.tlv[v] = m;
+  }
+  L.tw = tmem_base + ((uint32_t)(warp * 32) << 16);
+  L.Wf = (float)geom.W;
+  L.invW = 1.0f / (float)geom.W;
+#pragma unroll
+  for (int v = 0; v < 2; ++v) {
+    const int vl = L.vl0 + 8 * v;
     const int nc = geom.nc[vl], nt = geom.nt[vl];
     L.base[v] = geom.base[vl];
     L.tbase[v] = geom.tbase[vl];
+    L.basef[v] = (float)geom.base[vl];
+    L.tbasef[v] = (float)geom.tbase[vl];
     uint32_t own = 0u;
     for (int j = 0; j < L.ch + L.tl; ++j) {
       const bool o = j < L.ch ? j < nc : (j - L.ch) < nt;
@@ -478,8 +545,8 @@ __global__ void __launch_bounds__(l2::TPB, 4)
     }
     L.own[v] = own;
   }
-  // coordinate tables: thread vl < 16 writes its virtual lane's pairs and solo slots
-  if (tid < 16) {
+  // coordinate tables: thread vl < VL writes its virtual lane's pairs and solo slots
+  if (!l2::Smem<SL>::kGen && tid < VL) {
     const int vl = tid, nc = geom.nc[vl], nt = geom.nt[vl], base = geom.base[vl], tbase = geom.tbase[vl];
     auto xy = [&](int j) {
       const bool o = j < L.ch ? j < nc : (j - L.ch) < nt;
@@ -488,9 +555,9 @@ __global__ void __launch_bounds__(l2::TPB, 4)
     };
     for (int i = 0; i < S.np; ++i) {
       const float2 a = xy(2 * i), b = xy(2 * i + 1);
-      S.xy[i * 16 + vl] = make_float4(a.x, b.x, a.y, b.y);
+      S.xy[i * VL + vl] = make_float4(a.x, b.x, a.y, b.y);
     }
-    for (int s = 0; s < S.ns; ++s) S.sxy[s * 16 + vl] = xy((L.ch & ~1) + s);
+    for (int s = 0; s < S.ns; ++s) S.sxy[s * VL + vl] = xy((L.ch & ~1) + s);
   }
   if (tid == 0) {
     S.kc[0] = ddiv_rcp(cfg.lam_down);
@@ -506,7 +573,7 @@ __global__ void __launch_bounds__(l2::TPB, 4)
   double G = 0.0;
   LMState<3> s;
   s.sys = S.sys + L.gib * kSysQ;
-  s.gmask = 0xFFu << (lane & ~7);
+  s.gmask = LG == 32 ? kFull : ((1u << LG) - 1u) << (lane & ~(LG - 1));
   s.sys_writer = L.gl == 0;
   int64_t spot = -1;
   bool need = true, exhausted = false;
@@ -519,11 +586,11 @@ __global__ void __launch_bounds__(l2::TPB, 4)
   auto claim = [&](bool want) -> int64_t {
     unsigned long long v = 0ull;
     if (want && L.gl == 0) v = atomicAdd(wk, 1ull);
-    return (int64_t)__shfl_sync(kFull, v, lane & ~7);
+    return (int64_t)__shfl_sync(kFull, v, lane & ~(LG - 1));
   };
   auto prefetch = [&](int64_t sp) {
     if (sp < count) {
-      nsh = stage2l<PX>(S, L.gib, L.gl, images + sp * (int64_t)N, lo, hi, N);
+      nsh = stage2l<SL, PX>(S, L.gib, L.gl, images + sp * (int64_t)N, lo, hi, N);
 #pragma unroll
       for (int k = 0; k < 3; ++k) nxt[k] = __ldg(inits + sp * 3 + k);
     }
@@ -545,7 +612,7 @@ __global__ void __launch_bounds__(l2::TPB, 4)
       __syncwarp(kFull);
       const PX* win = reinterpret_cast<const PX*>(S.stage + L.gib * S.sw) + nsh;
       bool sgt, sg40;
-      const double gsum = load_spot2l<FULL, PX>(S, L, win, load, sgt, sg40);
+      const double gsum = load_spot2l<SL, FULL, PX>(S, L, win, load, sgt, sg40);
       bool bad = false;
       if (load) {
         float init[3];
@@ -591,7 +658,7 @@ __global__ void __launch_bounds__(l2::TPB, 4)
     }
     if (__all_sync(kFull, exhausted)) break;
     Eval<3> E;
-    evaluate2l<FULL>(S, L, G, n, s.p, warp_gt, lane_g40, !exhausted && !skip, geom.nz2, E);
+    evaluate2l<SL, FULL>(S, L, G, n, s.p, warp_gt, lane_g40, !exhausted && !skip, geom.nz2, E);
     if (!exhausted && !skip) {
       n_e += 1;
       if (lm_step<3>(s, E, cfg, out, spot, leader, N, n_g, n_t, S.kc)) need = true;

@@ -3,7 +3,8 @@
 // Chain / tail pixel counts are uniform runtime loop bounds (Geom::ch, tl), so
 // one kernel per (P, SLOTS) serves every grid with that pairwise-tree depth.
 #include "sf_launch.h"
-#if SF_P == 3 && SF_SLOTS == 2
+#if SF_P == 3 && (SF_SLOTS == 2 || SF_SLOTS == 4 || SF_SLOTS == 8)
+#define SF_HAS_FIT2L 1
 #include <cstdlib>
 
 #include "sf_fit2l.cuh"
@@ -18,26 +19,25 @@
 
 namespace sf {
 
-#if SF_P == 3 && SF_SLOTS == 2
-// Two-leaf spots with given inits (float or 16-bit pixels): the two-leaves-per-lane kernel with its
-// profile cache in Tensor Memory (sf_fit2l.cuh).  SPOTFIT_FIT2L=0 selects the general kernel.
+#ifdef SF_HAS_FIT2L
+// Symmetric spots of 2, 4 or 8 leaves with given inits (float or 16-bit pixels): the
+// two-leaves-per-lane kernel with its profile cache in Tensor Memory (sf_fit2l.cuh), when its
+// shared memory leaves room for four CTAs per SM.  SPOTFIT_FIT2L=0 selects the general kernel.
 template <typename PX>
 static int launch_fit2l(const LaunchFit& a, const PX* images, cudaError_t* err) {
-  auto kern = a.geom.full ? fit_kernel2l<true, PX> : fit_kernel2l<false, PX>;
-  const size_t smem = l2::Smem::bytes(a.geom.ch, a.geom.tl, a.geom.N);
+  auto kern = a.geom.full ? fit_kernel2l<SF_SLOTS, true, PX> : fit_kernel2l<SF_SLOTS, false, PX>;
+  const size_t smem = l2::Smem<SF_SLOTS>::bytes(a.geom.ch, a.geom.tl, a.geom.N);
   *err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (*err != cudaSuccess) return 0;
   *err = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (*err != cudaSuccess) return 0;
-  int per_sm = 0;
-  *err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, l2::TPB, smem);
-  if (*err != cudaSuccess) return 0;
   // TMEM: 512 columns per SM.  The occupancy API reports 1 CTA per SM for this kernel (it uses
-  // tcgen05); registers (128 x 128 threads), shared memory (< 57 KB) and TMEM (128 columns) all allow 4.
-  (void)per_sm;
-  per_sm = 512 / l2::kCols;
+  // tcgen05); registers (128 x 128 threads), shared memory (use_fit2l: <= 56 KB) and TMEM (128
+  // columns) all allow 4.
+  const int per_sm = 512 / l2::kCols;
+  constexpr int GPB = l2::groups_per_cta<SF_SLOTS>();
   int64_t blocks = (int64_t)per_sm * a.sm_count;
-  const int64_t need = (a.count + l2::GPB - 1) / l2::GPB;
+  const int64_t need = (a.count + GPB - 1) / GPB;
   if (blocks > need) blocks = need;
   if (blocks < 1) return 0;
   kern<<<(unsigned)blocks, l2::TPB, smem, a.stream>>>(images, a.inits, a.count, a.geom, a.cfg, a.out);
@@ -50,13 +50,14 @@ static bool use_fit2l(const LaunchFit& a) {
     const char* e = std::getenv("SPOTFIT_FIT2L");
     return !(e && e[0] == '0');
   }();
-  return on && a.inits != nullptr && a.geom.ch <= 2 * l2::kMaxPairs + 1;
+  return on && a.inits != nullptr && a.geom.ch <= 2 * l2::kMaxPairs &&
+         l2::Smem<SF_SLOTS>::bytes(a.geom.ch, a.geom.tl, a.geom.N) <= 56 * 1024;
 }
 #endif
 
 template <typename PX>
 static int launch_fit_px(const LaunchFit& a, const PX* images, cudaError_t* err) {
-#if SF_P == 3 && SF_SLOTS == 2
+#ifdef SF_HAS_FIT2L
   if (use_fit2l(a)) return launch_fit2l<PX>(a, images, err);
 #endif
   const bool fused = a.inits == nullptr;
