@@ -3,7 +3,7 @@
 // Chain / tail pixel counts are uniform runtime loop bounds (Geom::ch, tl), so
 // one kernel per (P, SLOTS) serves every grid with that pairwise-tree depth.
 #include "sf_launch.h"
-#if SF_P == 3 && (SF_SLOTS == 2 || SF_SLOTS == 4 || SF_SLOTS == 8)
+#if (SF_P == 3 || SF_P == 4) && (SF_SLOTS == 2 || SF_SLOTS == 4 || SF_SLOTS == 8)
 #define SF_HAS_FIT2L 1
 #include <cstdlib>
 
@@ -20,21 +20,22 @@
 namespace sf {
 
 #ifdef SF_HAS_FIT2L
-// Symmetric spots of 2, 4 or 8 leaves with given inits (float or 16-bit pixels): the
+// Spots of 2, 4 or 8 leaves with given inits (float or 16-bit pixels; symmetric or elliptical): the
 // two-leaves-per-lane kernel with its profile cache in Tensor Memory (sf_fit2l.cuh), when its
-// shared memory leaves room for four CTAs per SM.  SPOTFIT_FIT2L=0 selects the general kernel.
+// shared memory leaves room for its CTAs per SM (4 for P = 3, 3 for P = 4).  SPOTFIT_FIT2L=0 selects
+// the general kernel.
 template <typename PX>
 static int launch_fit2l(const LaunchFit& a, const PX* images, cudaError_t* err) {
-  auto kern = a.geom.full ? fit_kernel2l<SF_SLOTS, true, PX> : fit_kernel2l<SF_SLOTS, false, PX>;
-  const size_t smem = l2::Smem<SF_SLOTS>::bytes(a.geom.ch, a.geom.tl, a.geom.N);
+  auto kern = a.geom.full ? fit_kernel2l<SF_SLOTS, SF_P, true, PX> : fit_kernel2l<SF_SLOTS, SF_P, false, PX>;
+  const size_t smem = l2::Smem<SF_SLOTS, SF_P>::bytes(a.geom.ch, a.geom.tl, a.geom.N);
   *err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (*err != cudaSuccess) return 0;
   *err = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (*err != cudaSuccess) return 0;
   // TMEM: 512 columns per SM.  The occupancy API reports 1 CTA per SM for this kernel (it uses
-  // tcgen05); registers (128 x 128 threads), shared memory (use_fit2l: <= 56 KB) and TMEM (128
-  // columns) all allow 4.
-  const int per_sm = 512 / l2::kCols;
+  // tcgen05); registers (launch bound), shared memory (use_fit2l) and TMEM (128 columns) all allow
+  // minb2l CTAs.
+  const int per_sm = minb2l<SF_P>();
   constexpr int GPB = l2::groups_per_cta<SF_SLOTS>();
   int64_t blocks = (int64_t)per_sm * a.sm_count;
   const int64_t need = (a.count + GPB - 1) / GPB;
@@ -51,7 +52,7 @@ static bool use_fit2l(const LaunchFit& a) {
     return !(e && e[0] == '0');
   }();
   return on && a.inits != nullptr && a.geom.ch <= 2 * l2::kMaxPairs &&
-         l2::Smem<SF_SLOTS>::bytes(a.geom.ch, a.geom.tl, a.geom.N) <= 56 * 1024;
+         l2::Smem<SF_SLOTS, SF_P>::bytes(a.geom.ch, a.geom.tl, a.geom.N) + 1024 <= (size_t)228 * 1024 / minb2l<SF_P>();
 }
 #endif
 
