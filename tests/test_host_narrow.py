@@ -1,7 +1,6 @@
 """The host pipeline's lossless f32 -> u16 narrowing (csrc/sf_host_narrow.cpp, sf_debug_narrow_u16):
 a chunk crosses PCIe as u16 only when every pixel is an integer in [0, 65535] with a clear sign bit,
 and then the u16 values are exactly the pixels (the fit kernel widens them back exactly)."""
-import ctypes
 
 import numpy as np
 import pytest
