@@ -154,37 +154,60 @@ def cmd_assess(a):
     return 0
 
 
+REPEATS = {10: 200, 100: 20, 1000: 10, 10000: 1}  # PAPER.md Results: "run 200x, 20x, 10x and once"
+
+
+def bench_plan(sizes: str, batches: str, repeats: str = ""):
+    """SPEC.md:475-478 BenchPlan -> [(S, batch, repeats)]: sizes "4-32" (a range) or a comma list,
+    batch sizes with the paper's repeat counts unless given."""
+    if "-" in sizes:
+        lo, hi = (int(v) for v in sizes.split("-"))
+        S = list(range(lo, hi + 1))
+    else:
+        S = [int(v) for v in sizes.split(",")]
+    B = [int(v) for v in batches.split(",")]
+    R = [int(v) for v in repeats.split(",")] if repeats else [REPEATS.get(b, max(1, 2000 // b)) for b in B]
+    if any(s < 1 or s * s > 1024 for s in S) or any(b < 1 for b in B) or len(R) != len(B) or min(R) < 1:
+        raise CliError(EXIT_ARGS, "sizes must satisfy S*S <= 1024; batches and repeats >= 1, one repeat per batch")
+    return [(s, b, r) for s in S for b, r in zip(B, R)]
+
+
 def cmd_bench(a):
-    """SPEC.md:471-512 run_bench: per (S, batch) wall time of fit_batch from host memory
-    (marshaling + fit + result collection), inits excluded, after a warm-up call."""
+    """SPEC.md:471-512 run_bench: per (S, batch) mean wall time of fit_batch from host memory
+    (marshaling + fit + result collection), inits excluded, after a warm-up call; monotonic clock;
+    timings under 5 clock ticks are flagged."""
     from .batch_engine import fit_batch
     from .initializer import estimate_initial_batch
     from .model import PixelGrid
     from .simulator import SimConfig, simulate_batch
 
-    sizes = [int(s) for s in a.sizes.split(",")]
-    batches = [int(b) for b in a.batches.split(",")]
-    if any(s < 1 or s * s > 1024 for s in sizes) or any(b < 1 for b in batches):
-        raise CliError(EXIT_ARGS, "sizes must satisfy S*S <= 1024, batches >= 1")
+    plan = bench_plan(a.sizes, a.batches, a.repeats)
+    tick = time.get_clock_info("perf_counter").resolution
     entries = []
-    for S in sizes:
+    for S, B, reps in plan:
         grid = PixelGrid(S, S)
-        for B in batches:
-            im, _ = simulate_batch(SimConfig(width=S, height=S, count=B, seed=S * 1000 + B,
-                                             n_signal=a.signal, n_background=a.background))
-            flat = im.reshape(B, S * S)
-            ini = estimate_initial_batch(flat, 3, grid=grid)[0]
-            fit_batch(flat, ini, grid=grid)  # warm-up
-            reps = max(1, min(200, int(1e5 // B)))
-            t0 = time.perf_counter()
-            for _ in range(reps):
-                fit_batch(flat, ini, grid=grid)
-            dt = (time.perf_counter() - t0) / reps
-            entries.append({"size": S, "batch": B, "repeats": reps, "seconds_per_call": dt, "fits_per_s": B / dt,
-                            "pixels_per_s": B * S * S / dt})
+        im, _ = simulate_batch(SimConfig(width=S, height=S, count=B, seed=S * 1000 + B, n_signal=a.signal,
+                                         n_background=a.background))
+        flat = im.reshape(B, S * S)
+        ini, amps = estimate_initial_batch(flat, 3, grid=grid)
+        if a.engine == "explicit5":  # (x, y, sigma) + the initializer's (alpha, beta), SPEC.md:271
+            ini = np.ascontiguousarray(np.concatenate([ini, amps], axis=1), dtype=np.float32)
+        fit_batch(flat, ini, grid=grid, engine=a.engine)  # warm-up
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            fit_batch(flat, ini, grid=grid, engine=a.engine)
+        dt = (time.perf_counter() - t0) / reps
+        entries.append({"size": S, "batch": B, "repeats": reps, "seconds_per_call": dt, "fits_per_s": B / dt,
+                        "pixels_per_s": B * S * S / dt, "under_resolved": dt < 5 * tick})
     import torch
 
-    _dump({"machine": torch.cuda.get_device_name(0), "engine": "implicit3/cuda", "entries": entries}, a.report)
+    _dump({"machine": torch.cuda.get_device_name(0), "engine": a.engine + "/cuda", "entries": entries}, a.report)
+    if a.csv:
+        with open(a.csv, "w") as f:
+            f.write("size,batch,repeats,seconds_per_call,fits_per_s,pixels_per_s\n")
+            for e in entries:
+                f.write(f"{e['size']},{e['batch']},{e['repeats']},{e['seconds_per_call']!r},{e['fits_per_s']!r},"
+                        f"{e['pixels_per_s']!r}\n")
     return 0
 
 
@@ -226,8 +249,10 @@ def build_parser():
     a.add_argument("--signal", type=float, default=0.0)
     a.add_argument("--max-iter", type=int, default=20, help="histogram range (the fit's --max-iter)")
     b = sub.add_parser("bench")
-    b.add_argument("--sizes", default="4,9,16,25,32")
+    b.add_argument("--sizes", default="4-32", help="range lo-hi or a comma list (SPEC.md:475: S = 4..32)")
     b.add_argument("--batches", default="10,100,1000,10000")
+    b.add_argument("--repeats", default="", help="per batch size (default 200, 20, 10, 1 as the paper)")
+    b.add_argument("--csv", default="", help="optional CSV table, one row per (S, batch)")
     b.add_argument("--signal", type=float, default=400.0)
     b.add_argument("--background", type=float, default=40.0)
     b.add_argument("--engine", default="implicit3")

@@ -159,3 +159,33 @@ def test_cli_flags_column_feeds_assess(tmp_path):
     assert r["iterations"]["no_improvement"] == int(((got["flags"] & 0x80) != 0).sum())
     assert r2["iterations"]["no_improvement"] is None  # unavailable without the column, not a false 0
     assert r["accuracy"] == r2["accuracy"]
+
+
+def test_bench_default_plan_is_the_papers():
+    """S = 4..32 x batches 10/100/1000/10000 -> 29 * 4 = 116 entries, repeated
+    200x, 20x, 10x and once."""
+    from paper_2106_02045_b200.cli import CliError, bench_plan, build_parser
+
+    a = build_parser().parse_args(["bench"])
+    plan = bench_plan(a.sizes, a.batches, a.repeats)
+    assert len(plan) == 116
+    assert {(b, r) for _, b, r in plan} == {(10, 200), (100, 20), (1000, 10), (10000, 1)}
+    assert sorted({s for s, _, _ in plan}) == list(range(4, 33))
+    with pytest.raises(CliError):
+        bench_plan("33", "10")
+
+
+@pytest.mark.gpu
+def test_cli_bench_report(tmp_path):
+    """run_bench report identities: fits/s * time = batch, pixels/s = fits/s * S^2."""
+    from paper_2106_02045_b200.cli import main
+
+    rep, csv = tmp_path / "b.json", tmp_path / "b.csv"
+    assert main(["bench", "--sizes", "9,16", "--batches", "10,1000", "--repeats", "3,2", "--report", str(rep),
+                 "--csv", str(csv)]) == 0
+    r = json.load(open(rep))
+    assert len(r["entries"]) == 4 and "B200" in r["machine"]
+    for e in r["entries"]:
+        assert abs(e["fits_per_s"] * e["seconds_per_call"] - e["batch"]) < 1e-6 * e["batch"]
+        assert abs(e["pixels_per_s"] - e["fits_per_s"] * e["size"] ** 2) < 1e-6 * e["pixels_per_s"]
+    assert len(open(csv).read().splitlines()) == 5
