@@ -542,7 +542,10 @@ __device__ __forceinline__ int stage2l(const Smem<SL, P>& S, int gib, int gl, co
 
 // launch bound: 4 CTAs per SM (128 registers) for P = 3; 3 for the elliptical model
 template <int P>
-__host__ __device__ constexpr int minb2l() { return P == 3 ? 4 : 3; }
+#ifndef SF_MINB2L_P3
+#define SF_MINB2L_P3 4
+#endif
+__host__ __device__ constexpr int minb2l() { return P == 3 ? SF_MINB2L_P3 : 3; }
 
 // The kernel: fit_kernel's loop (refill -> fused evaluation -> LM step) for spots of SL leaves with
 // given inits; PX: float pixels or 16-bit counts (staged as u16, widened exactly in load_spot2l).
