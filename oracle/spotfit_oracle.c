@@ -19,7 +19,7 @@
  *                    chi_squared, gradient_sums, coefficient_gradients,
  *                    chi_gradient) + the normal matrix of SPEC.md:173-176.
  *                    Pinned bit-for-bit against the reference model.py via
- *                    tests/golden/*.npz (tests/golden/make_golden.py).
+ *                    the tests/golden npz fixtures (tests/golden/make_golden.py).
  *   sf_oracle_fit    LM state machine of PAPER.md:126-180 / SPEC.md:209-262 as
  *                    pinned in SURVEY.md App. A (and DESIGN.md section 3).
  *   elliptical (P=4) SURVEY.md App. B.5 -- no reference exists (SPEC.md:152
@@ -336,7 +336,7 @@ static int solve_pivot5(const double* jtj, const double* rhs, double lam, double
 
 int sf_oracle_solve(int P, const double* jtj, const double* rhs, double lam, double* delta) {
   if (P == 5) return solve_pivot5(jtj, rhs, lam, delta);
-  double A[4][4], L[4][4], C[4][4], D[4], z[4];
+  double A[4][4] = {{0}}, L[4][4] = {{0}}, C[4][4] = {{0}}, D[4] = {0}, z[4] = {0};
   for (int i = 0; i < P; ++i)
     for (int j = 0; j < P; ++j) A[i][j] = jtj[sym_idx(P, i, j)];
   for (int i = 0; i < P; ++i) A[i][i] = A[i][i] + lam * A[i][i];
