@@ -47,11 +47,17 @@ static int launch_fit2l(const LaunchFit& a, const PX* images, cudaError_t* err) 
 }
 
 static bool use_fit2l(const LaunchFit& a) {
-  static const bool on = [] {
+  // SPOTFIT_FIT2L: 0 = never, 1 (default) = from one full wave upward, 2 = always (validation)
+  static const int mode = [] {
     const char* e = std::getenv("SPOTFIT_FIT2L");
-    return !(e && e[0] == '0');
+    return e ? (int)std::strtol(e, nullptr, 10) : 1;
   }();
-  return on && a.inits != nullptr && a.geom.ch <= 2 * l2::kMaxPairs &&
+  const bool on = mode > 0;
+  // A batch smaller than one full wave of the kernel (every group of every CTA busy) finishes faster
+  // on the general kernel, whose spots walk both leaves in parallel lanes (lower latency per spot):
+  // the two-leaf kernel pays off when spots queue up.
+  const int64_t wave = (int64_t)a.sm_count * minb2l<SF_P>() * l2::groups_per_cta<SF_SLOTS>();
+  return on && a.inits != nullptr && (a.count >= wave || mode >= 2) && a.geom.ch <= 2 * l2::kMaxPairs &&
          l2::Smem<SF_SLOTS, SF_P>::bytes(a.geom.ch, a.geom.tl, a.geom.N) + 1024 <= (size_t)228 * 1024 / minb2l<SF_P>();
 }
 #endif

@@ -2,7 +2,7 @@
 Memory) and the general kernel (sf_fit_kernel.cuh, SPOTFIT_FIT2L=0) give bit-identical fits on every
 geometry family the former serves: 2, 4 and 8 leaves, symmetric and elliptical, full and ragged
 chains, float and 16-bit pixels.  The selector is read once per process, so each kernel runs in its
-own subprocess."""
+own subprocess (SPOTFIT_FIT2L=2 forces the two-leaf kernel below its one-wave threshold)."""
 import os
 import subprocess
 import sys
@@ -42,7 +42,7 @@ def run(tmp_path, fit2l):
 
 
 def test_two_leaf_kernel_equals_general_kernel(tmp_path):
-    a, b = run(tmp_path, 1), run(tmp_path, 0)
+    a, b = run(tmp_path, 2), run(tmp_path, 0)
     assert sorted(a.files) == sorted(b.files)
     bad = [k for k in a.files if not np.array_equal(a[k].view(np.uint8), b[k].view(np.uint8))]
     assert not bad, bad[:10]
