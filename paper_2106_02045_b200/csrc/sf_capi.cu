@@ -235,6 +235,8 @@ struct DevCtx {
   int sms = 1;
   Slot slot[kStreams];
   unsigned long long* d_evals = nullptr;
+  unsigned long long* h_evals = nullptr;  // pinned: the evaluation counters read back with the results
+  cudaEvent_t evals_zeroed = nullptr;     // the counter reset, which every slot stream waits for
 };
 
 std::mutex g_ctx_mu;
@@ -267,6 +269,8 @@ int ensure_ctx(DevCtx& c, int dev, size_t spots, int npix, int P, bool staging, 
       for (auto& e : s.ev) SF_CUDA(cudaEventCreate(&e));
     }
     SF_CUDA(cudaMalloc(&c.d_evals, 3 * sizeof(unsigned long long)));
+    SF_CUDA(cudaHostAlloc(&c.h_evals, 3 * sizeof(unsigned long long), cudaHostAllocPortable));
+    SF_CUDA(cudaEventCreateWithFlags(&c.evals_zeroed, cudaEventDisableTiming));
     c.init = true;
   }
   for (auto& s : c.slot) {
@@ -445,8 +449,10 @@ int run_shard(int dev, HostJob& j) {
   }();
   const bool narrow = narrow_env > 0 && !j.images16 && j.images != nullptr && (!j.pinned_in || narrow_env > 1);
   if (ensure_ctx(*c, dev, (size_t)chunk, N, P, staging, narrow) != 0) return -1;
+  // reset the evaluation counters; the other slot streams wait on the device, not the host
   SF_CUDA(cudaMemsetAsync(c->d_evals, 0, 3 * sizeof(unsigned long long), c->slot[0].stream));
-  SF_CUDA(cudaStreamSynchronize(c->slot[0].stream));
+  SF_CUDA(cudaEventRecord(c->evals_zeroed, c->slot[0].stream));
+  for (int k = 1; k < kStreams; ++k) SF_CUDA(cudaStreamWaitEvent(c->slot[k].stream, c->evals_zeroed, 0));
   // SPOTFIT_TRACE=1: per-chunk device timeline on stderr (diagnostic; tools/e2e_sweep.py)
   static const bool trace = std::getenv("SPOTFIT_TRACE") != nullptr;
   std::vector<cudaEvent_t> tev;
@@ -549,6 +555,11 @@ int run_shard(int dev, HostJob& j) {
     SF_CUDA(mark(s.stream));
     ++j.chunks;
   }
+  // the counters follow every chunk's fit: slot 0 waits for the other slots' last events, then
+  // copies them back with its own results (no separate blocking copy afterwards)
+  for (int k = 1; k < kStreams; ++k) SF_CUDA(cudaStreamWaitEvent(c->slot[0].stream, c->slot[k].ev[3], 0));
+  SF_CUDA(cudaMemcpyAsync(c->h_evals, c->d_evals, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                          c->slot[0].stream));
   for (auto& s : c->slot) {
     SF_CUDA(cudaStreamSynchronize(s.stream));
     if (staging) copy_out_staged(s, j);
@@ -561,7 +572,7 @@ int run_shard(int dev, HostJob& j) {
     }
     for (auto e : tev) cudaEventDestroy(e);
   }
-  SF_CUDA(cudaMemcpy(j.evals, c->d_evals, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  for (int k = 0; k < 3; ++k) j.evals[k] = c->h_evals[k];
   return 0;
 }
 

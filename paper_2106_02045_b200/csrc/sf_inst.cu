@@ -14,10 +14,64 @@
 #error "compile with -DSF_P=3|4 -DSF_SLOTS=1|2|4|8|16"
 #endif
 
+#include <mutex>
+#include <vector>
+
 #define SF_CAT5(a, b, c, d, e) a##b##c##d##e
 #define SF_UNIT_NAME(kind, P, S) SF_CAT5(kind, _P, P, _S, S)
 
 namespace sf {
+
+// Launch setup done once per (kernel, device, shared-memory size) instead of on every launch --
+// small batches are latency-bound, and these are driver calls: the dynamic shared-memory attribute
+// (raised to the largest size seen for the kernel on the device, so it always covers smem) and the
+// occupancy query (query = false skips it).
+static cudaError_t prepare_kernel(const void* kern, int tpb, size_t smem, int* per_sm, bool query) {
+  struct Attr {
+    const void* kern;
+    int dev;
+    size_t max_smem;
+  };
+  struct Occ {
+    const void* kern;
+    int dev;
+    size_t smem;
+    int per_sm;
+  };
+  static std::mutex mu;
+  static std::vector<Attr> attrs;
+  static std::vector<Occ> occs;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  Attr* at = nullptr;
+  for (Attr& x : attrs)
+    if (x.kern == kern && x.dev == dev) at = &x;
+  if (at == nullptr || at->max_smem < smem) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
+    if (at == nullptr)
+      attrs.push_back(Attr{kern, dev, smem});
+    else
+      at->max_smem = smem;
+  }
+  *per_sm = 1;
+  if (!query) return cudaSuccess;
+  for (const Occ& x : occs)
+    if (x.kern == kern && x.dev == dev && x.smem == smem) {
+      *per_sm = x.per_sm;
+      return cudaSuccess;
+    }
+  int n = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, tpb, smem);
+  if (e != cudaSuccess) return e;
+  occs.push_back(Occ{kern, dev, smem, n});
+  *per_sm = n;
+  return cudaSuccess;
+}
 
 #ifdef SF_HAS_FIT2L
 // Spots of 2, 4 or 8 leaves with given inits (float or 16-bit pixels; symmetric or elliptical): the
@@ -28,9 +82,8 @@ template <typename PX>
 static int launch_fit2l(const LaunchFit& a, const PX* images, cudaError_t* err) {
   auto kern = a.geom.full ? fit_kernel2l<SF_SLOTS, SF_P, true, PX> : fit_kernel2l<SF_SLOTS, SF_P, false, PX>;
   const size_t smem = l2::Smem<SF_SLOTS, SF_P>::bytes(a.geom.ch, a.geom.tl, a.geom.N);
-  *err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (*err != cudaSuccess) return 0;
-  *err = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  int unused = 0;
+  *err = prepare_kernel((const void*)kern, l2::TPB, smem, &unused, false);
   if (*err != cudaSuccess) return 0;
   // TMEM: 512 columns per SM.  The occupancy API reports 1 CTA per SM for this kernel (it uses
   // tcgen05); registers (launch bound), shared memory (use_fit2l) and TMEM (128 columns) all allow
@@ -73,10 +126,8 @@ static int launch_fit_px(const LaunchFit& a, const PX* images, cudaError_t* err)
   constexpr int tpb = threads_per_block<SF_SLOTS>();
   constexpr int groups_per_block = SF_SLOTS >= 8 ? 1 : (tpb / 32) * (32 / (8 * SF_SLOTS));
   const size_t smem = Smem<SF_P, SF_SLOTS>::bytes(a.geom.ch, a.geom.tl, a.geom.N);
-  *err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (*err != cudaSuccess) return 0;
   int per_sm = 0;
-  *err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, tpb, smem);
+  *err = prepare_kernel((const void*)kern, tpb, smem, &per_sm, true);
   if (*err != cudaSuccess) return 0;
   if (per_sm < 1) per_sm = 1;
   int64_t blocks = (int64_t)per_sm * a.sm_count;
