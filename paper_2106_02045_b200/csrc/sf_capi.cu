@@ -415,7 +415,10 @@ int run_shard(int dev, HostJob& j) {
   // the tail halves down to kMinChunk so that the kernel + D2H of the last chunk, which run
   // after the final H2D, are short.  Three streams overlap H2D(k+1) with kernel(k).
   const size_t px_bytes_in = j.images16 ? sizeof(uint16_t) : sizeof(float);
-  const int64_t kMinChunk = 16384;
+  // smallest chunk: total / 8 within [2048, 16384] spots, so that mid-size batches (1e4..1e5 spots)
+  // still pipeline copy and fit over a few chunks (tools/call_overhead.py: 3e4 pageable spots
+  // 1.81 -> 1.43 ms) while large ones keep 16384-spot tails
+  const int64_t kMinChunk = std::min<int64_t>(16384, std::max<int64_t>(2048, total / 8));
   // chunk caps (MB of input per H2D), measured with tools/e2e_sweep.py on a B200 (PCIe Gen5 x16):
   // f32 input is copy-bound and flat above ~64 MB (96 MB best); u16 input is kernel-bound and
   // wants short chunks so that the first kernel starts early.  SPOTFIT_CHUNK_MB[16] override.
