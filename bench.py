@@ -100,22 +100,31 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled during the timed region.  nvidia-smi takes a few
+    hundred ms to start, longer than a 20-step timed region, so the sampler is started (and its first
+    row awaited) before the warm-up; rows carry the host time they arrived, and the summary keeps the
+    rows inside the timed window (+- one sampling period), else the rows bracketing it."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    PERIOD_S = 0.1
 
     def __init__(self, gpus):
         self.gpus, self.rows, self.proc = sorted(set(gpus)), [], None
+        self.t0 = self.t1 = None
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", ",".join(str(g) for g in self.gpus),
-                                          f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "100"],
+                                          f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms",
+                                          str(int(self.PERIOD_S * 1000))],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            deadline = time.monotonic() + 3.0
+            while not self.rows and time.monotonic() < deadline:  # the sampler is live before timing starts
+                time.sleep(0.01)
         except OSError:
             self.proc = None
         return self
@@ -124,7 +133,15 @@ class ClockSampler:
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) == 7:
-                self.rows.append(parts)
+                self.rows.append((time.monotonic(), parts))
+
+    def begin(self):
+        self.t0 = time.monotonic()
+
+    def end(self):
+        self.t1 = time.monotonic()
+        # one more sampling period so the rows covering the end of the window arrive
+        time.sleep(1.5 * self.PERIOD_S)
 
     def __exit__(self, *a):
         if self.proc:
@@ -135,14 +152,27 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        if not self.rows:
+        rows = self.rows
+        how = "in the timed window"
+        if self.t0 is not None and self.t1 is not None:
+            inside = [r for t, r in rows if self.t0 - self.PERIOD_S <= t <= self.t1 + self.PERIOD_S]
+            if not inside:  # the rows on either side of the window
+                before = [r for t, r in rows if t < self.t0][-1:]
+                after = [r for t, r in rows if t > self.t1][:1]
+                inside = before + after
+                how = "bracketing the timed window"
+            rows = inside
+        else:
+            rows = [r for _, r in rows]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(rows), "sampled": how,
+                "window_s": None if self.t0 is None else self.t1 - self.t0}
 
 
 def load_peaks():
@@ -408,14 +438,6 @@ class KernelLeg:
         return {"params": par, "alpha": f[0], "beta": f[1], "nchi2": f[2], "status": u8[0], "iterations": u8[1]}
 
 
-class _Null:
-    def __enter__(self):
-        return self
-
-    def __exit__(self, *a):
-        return False
-
-
 def time_legs(legs, steps, warmup, devs, clock=None):
     """Launch every leg `steps` times (all devices concurrently), CUDA events on each launching
     stream; -> (max ms over devices and ranks, per-device ms)."""
@@ -430,17 +452,20 @@ def time_legs(legs, steps, warmup, devs, clock=None):
         lg.d_ev.zero_()
         torch.cuda.synchronize(lg.dev)
     devs.barrier()
-    with clock if clock is not None else _Null():
+    if clock is not None:
+        clock.begin()
+    for lg in legs:
+        lg.e0.record(lg.stream)
+    for _ in range(steps):
         for lg in legs:
-            lg.e0.record(lg.stream)
-        for _ in range(steps):
-            for lg in legs:
-                with torch.cuda.device(lg.dev):
-                    lg.launch()
-        for lg in legs:
-            lg.e1.record(lg.stream)
-        for lg in legs:
-            lg.stream.synchronize()
+            with torch.cuda.device(lg.dev):
+                lg.launch()
+    for lg in legs:
+        lg.e1.record(lg.stream)
+    for lg in legs:
+        lg.stream.synchronize()
+    if clock is not None:
+        clock.end()
     devs.barrier()
     per = [lg.e0.elapsed_time(lg.e1) for lg in legs]
     return devs.max(max(per)), per
@@ -505,7 +530,8 @@ def run_ours(args):
     setup_s = time.perf_counter() - t0
     legs = [KernelLeg(sf, d, W, H, count, model, d_img, d_ini) for d, _, d_img, d_ini in batches]
     clock = ClockSampler(devs.ids)
-    ms_max, per_dev = time_legs(legs, args.steps, args.warmup, devs, clock)
+    with clock:  # started (and live) before the warm-up; the summary keeps the timed window's rows
+        ms_max, per_dev = time_legs(legs, args.steps, args.warmup, devs, clock)
     value = devs.n_gpus * count * args.steps / (ms_max * 1e-3)
     evs = [v / max(1, args.steps) for v in legs[0].d_ev.cpu().tolist()]  # per launch (= per step), device 0
     if args.profile:  # ncu / quick-look runs: kernel leg only (numbers taken under a profiler are not bench values)

@@ -26,7 +26,8 @@ namespace sf {
 // small batches are latency-bound, and these are driver calls: the dynamic shared-memory attribute
 // (raised to the largest size seen for the kernel on the device, so it always covers smem) and the
 // occupancy query (query = false skips it).
-static cudaError_t prepare_kernel(const void* kern, int tpb, size_t smem, int* per_sm, bool query) {
+static cudaError_t prepare_kernel(const void* kern, int tpb, size_t smem, int* per_sm, bool query,
+                                  bool max_carveout = false) {
   struct Attr {
     const void* kern;
     int dev;
@@ -51,8 +52,11 @@ static cudaError_t prepare_kernel(const void* kern, int tpb, size_t smem, int* p
   if (at == nullptr || at->max_smem < smem) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (e != cudaSuccess) return e;
+    if (max_carveout) {  // all of L1 as shared memory (the two-leaf kernel's 4 x 54 KB); the general
+                         // kernel keeps the driver's choice (its explicit-5 spills want L1)
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      if (e != cudaSuccess) return e;
+    }
     if (at == nullptr)
       attrs.push_back(Attr{kern, dev, smem});
     else
@@ -83,7 +87,7 @@ static int launch_fit2l(const LaunchFit& a, const PX* images, cudaError_t* err) 
   auto kern = a.geom.full ? fit_kernel2l<SF_SLOTS, SF_P, true, PX> : fit_kernel2l<SF_SLOTS, SF_P, false, PX>;
   const size_t smem = l2::Smem<SF_SLOTS, SF_P>::bytes(a.geom.ch, a.geom.tl, a.geom.N);
   int unused = 0;
-  *err = prepare_kernel((const void*)kern, l2::TPB, smem, &unused, false);
+  *err = prepare_kernel((const void*)kern, l2::TPB, smem, &unused, false, true);
   if (*err != cudaSuccess) return 0;
   // TMEM: 512 columns per SM.  The occupancy API reports 1 CTA per SM for this kernel (it uses
   // tcgen05); registers (launch bound), shared memory (use_fit2l) and TMEM (128 columns) all allow
