@@ -103,6 +103,9 @@ static int launch_fit2l(const LaunchFit& a, const PX* images, cudaError_t* err) 
   return (int)blocks;
 }
 
+#ifndef SF_FIT2L_WAVES
+#define SF_FIT2L_WAVES 1
+#endif
 static bool use_fit2l(const LaunchFit& a) {
   // SPOTFIT_FIT2L: 0 = never, 1 (default) = from one full wave upward, 2 = always (validation)
   static const int mode = [] {
@@ -113,7 +116,7 @@ static bool use_fit2l(const LaunchFit& a) {
   // A batch smaller than one full wave of the kernel (every group of every CTA busy) finishes faster
   // on the general kernel, whose spots walk both leaves in parallel lanes (lower latency per spot):
   // the two-leaf kernel pays off when spots queue up.
-  const int64_t wave = (int64_t)a.sm_count * minb2l<SF_P>() * l2::groups_per_cta<SF_SLOTS>();
+  const int64_t wave = (int64_t)a.sm_count * minb2l<SF_P>() * l2::groups_per_cta<SF_SLOTS>() * SF_FIT2L_WAVES;
   return on && a.inits != nullptr && (a.count >= wave || mode >= 2) && a.geom.ch <= 2 * l2::kMaxPairs &&
          l2::Smem<SF_SLOTS, SF_P>::bytes(a.geom.ch, a.geom.tl, a.geom.N) + 1024 <= (size_t)228 * 1024 / minb2l<SF_P>();
 }
