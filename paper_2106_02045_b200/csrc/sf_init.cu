@@ -23,6 +23,41 @@ namespace {
 // walk of sf_init_core.cuh; any other spot the general f64 scan.
 constexpr int kInitWarps = 8;
 
+#ifndef SF_INIT_PAIR
+#define SF_INIT_PAIR 1  // L < W <= 2L: a lane walks two adjacent columns off one set of row loads
+#endif
+#ifndef SF_INIT_CCOUNT
+#define SF_INIT_CCOUNT 1  // M of a tame spot over its contiguous pixels with 16-byte loads
+#endif
+#ifndef SF_INIT_TMA
+#define SF_INIT_TMA 1  // stage a task's window with one bulk async copy (mbarrier completion)
+#endif
+
+// Bulk async copy (the TMA engine's non-tensor form) and its mbarrier.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_addr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_addr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT;\n}\n" ::"r"(
+          smem_addr(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_to_smem(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(b))
+               : "memory");
+}
+
 template <typename PX>
 __host__ __device__ constexpr int init_buf_elems(int G, int N) {
   // the 16-B aligned window around G*N pixels, in PX units (+ one 16-B line of slack each side)
@@ -40,7 +75,7 @@ struct TameCol {
 };
 
 // Column k (0 or 1) of lane gl: when W <= L one column per lane, split into S row segments when
-// W < L / 2; when L < W <= 2L two full-height columns per lane (x = gl and gl + L).
+// W < L / 2; when L < W <= 2L two adjacent full-height columns per lane (x = 2 gl + k).
 template <int L>
 __device__ __forceinline__ TameCol tame_col(int W, int H, int gl, int k) {
   TameCol c;
@@ -53,7 +88,11 @@ __device__ __forceinline__ TameCol tame_col(int W, int H, int gl, int k) {
     c.y0 = seg * H / S;
     c.y1 = (seg + 1) * H / S;
   } else {
+#if SF_INIT_PAIR
+    c.x = 2 * gl + k;  // adjacent columns: walk_pair shares the row loads
+#else
     c.x = gl + k * L;
+#endif
     c.active = c.x < W;
     c.y0 = 0;
     c.y1 = H;
@@ -187,6 +226,214 @@ __device__ __forceinline__ int count_columns(const PX* st, int W, const TameCol 
   return r;
 }
 
+// Two adjacent columns x = cs[0].x and x + 1 of one lane (L < W <= 2L), in lockstep: a row's four
+// loads r[-1 .. 2] give both columns' horizontal 3-sums (four shared loads per row instead of six),
+// otherwise walk_tame<2>'s arithmetic (integer sums exact in any order).  Column x + 1 exists iff
+// liveB (= x < W - 1); without it its values are dropped from the scan and the tame check.
+template <typename PX>
+__device__ __forceinline__ void walk_pair(const PX* st, int W, int H, const TameCol (&cs)[2], bool liveB, InitScan& a,
+                                          bool& tame) {
+  using Acc = typename TameAcc<PX>::T;
+  const int x = cs[0].x;
+  const bool hlA = x > 0, hrB = x + 2 < W;
+  unsigned mx = 0u;
+  bool frac = false;
+  float lo = a.lo, best0 = -1.0f, best1 = -1.0f;
+  int brow0 = 0, brow1 = 0;
+  auto row = [&](const PX* r, Acc& hA, Acc& hB) {
+    const PX l = r[-1], c0 = r[0], c1 = r[1], rr = r[2];
+    if constexpr (sizeof(PX) == 4) {
+      const float f0 = (float)c0, f1 = liveB ? (float)c1 : 0.0f;
+      mx = max(mx, max(__float_as_uint(f0), __float_as_uint(f1)));
+      frac |= (__fsub_rn(__fadd_rn(f0, 8388608.0f), 8388608.0f) != f0) |
+              (__fsub_rn(__fadd_rn(f1, 8388608.0f), 8388608.0f) != f1);
+    }
+    hA = ((Acc)c0 + (hlA ? (Acc)l : (Acc)0)) + (liveB ? (Acc)c1 : (Acc)0);
+    hB = ((Acc)c1 + (Acc)c0) + (hrB ? (Acc)rr : (Acc)0);
+  };
+  auto take = [&](float vA, float vB, int y) {
+    if (vA > best0) {
+      best0 = vA;
+      brow0 = y;
+    }
+    if (vB > best1) {
+      best1 = vB;
+      brow1 = y;
+    }
+    lo = fminf(lo, liveB ? fminf(vA, vB) : vA);
+  };
+  const PX* p = st + x;
+  Acc pA = (Acc)0, pB = (Acc)0, cA, cB, nA, nB;
+  row(p, cA, cB);
+  int y = 0;
+  {  // top grid row
+    if (H > 1) row(p + W, nA, nB);
+    else nA = nB = (Acc)0;
+    take(tame_div((float)(pA + cA + nA), cs[0].ce, cs[0].rce), tame_div((float)(pB + cB + nB), cs[1].ce, cs[1].rce), 0);
+    pA = cA; pB = cB; cA = nA; cB = nB;
+    p += W;
+    ++y;
+  }
+#pragma unroll 2
+  for (; y < H - 1; ++y) {
+    row(p + W, nA, nB);
+    take(tame_div((float)(pA + cA + nA), cs[0].ci, cs[0].rci), tame_div((float)(pB + cB + nB), cs[1].ci, cs[1].rci), y);
+    pA = cA; pB = cB; cA = nA; cB = nB;
+    p += W;
+  }
+  if (y < H)  // bottom grid row (y = H - 1 > 0)
+    take(tame_div((float)(pA + cA), cs[0].ce, cs[0].rce), tame_div((float)(pB + cB), cs[1].ce, cs[1].rce), y);
+  unsigned long long key = key_max(a.key, scan_key(best0, brow0 * W + x));
+  if (liveB) key = key_max(key, scan_key(best1, brow1 * W + x + 1));
+  a.key = key;
+  a.lo = lo;
+  if constexpr (sizeof(PX) == 4) tame = tame && mx <= 0x49800000u && !frac;
+}
+
+// walk_pair for f32 pixels with the two columns in the halves of f32x2 registers: the horizontal
+// sums, the vertical sums, the tame check's rounding and tame_div run as FADD2 / FFMA2 / FMUL2 (the
+// same IEEE operation on each half).  A missing neighbour (grid edge, or column x + 1 when !liveB)
+// is read from the row's own pixel x and multiplied by 0: exact, and finite whenever the spot is tame
+// (a tame spot's pixels are integers), so nothing from outside the spot can reach a tame result.
+__device__ __forceinline__ void walk_pair_f32(const float* st, int W, int H, const TameCol (&cs)[2], bool liveB,
+                                              InitScan& a, bool& tame) {
+  const int x = cs[0].x;
+  // neighbour offsets of the top and bottom grid rows, where a missing neighbour would lie outside
+  // the spot; inside the grid the row above / below is the same spot's, so the interior rows read at
+  // constant offsets -1 .. 2 and the 0 factor alone drops a missing neighbour
+  const int oL = x > 0 ? -1 : 0, o1 = liveB ? 1 : 0, o2 = x + 2 < W ? 2 : 0;
+  const f2 mL = pk2(x > 0 ? 1.0f : 0.0f, 1.0f), mR = pk2(liveB ? 1.0f : 0.0f, x + 2 < W ? 1.0f : 0.0f);
+  const f2 nci = pk2(-cs[0].ci, -cs[1].ci), rci = pk2(cs[0].rci, cs[1].rci);
+  const f2 nce = pk2(-cs[0].ce, -cs[1].ce), rce = pk2(cs[0].rce, cs[1].rce);
+  const f2 big = bc2(8388608.0f), nbig = bc2(-8388608.0f), nz = bc2(-0.0f);
+  unsigned mx = 0u, fr = 0u;
+  float loA = a.lo, loB = a.lo, best0 = -1.0f, best1 = -1.0f;
+  int brow0 = 0, brow1 = 0;
+  auto hsum = [&](float l, float c0, float c1, float rr) -> f2 {
+    mx = __vimax3_u32(mx, __float_as_uint(c0), __float_as_uint(c1));
+    const f2 c = pk2(c0, c1);
+    // tame check: __fsub_rn(__fadd_rn(g, 2^23), 2^23) == g bitwise for both halves (-0.0 fails it,
+    // as it fails the bound on mx)
+    const f2 i = add2(add2(c, big), nbig);
+    fr |= (unsigned)(i.v ^ c.v) | (unsigned)((i.v ^ c.v) >> 32);
+    return fma2(pk2(c1, rr), mR, fma2(pk2(l, c0), mL, c));  // (g + l [x > 0]) + r [x < W - 1] per half
+  };
+  auto row_edge = [&](const float* r) { return hsum(r[oL], r[0], r[o1], r[o2]); };
+  auto row = [&](const float* r) { return hsum(r[-1], r[0], r[1], r[2]); };
+  auto div = [&](f2 sum, f2 nc, f2 rc) -> f2 {  // tame_div per half
+    const f2 q0 = mul2(sum, rc, nz);
+    return fma2(fma2(q0, nc, sum), rc, q0);
+  };
+  auto take = [&](f2 v, int y) {
+    float vA, vB;
+    up2(v, vA, vB);
+    if (vA > best0) {
+      best0 = vA;
+      brow0 = y;
+    }
+    if (vB > best1) {
+      best1 = vB;
+      brow1 = y;
+    }
+    loA = fminf(loA, vA);
+    loB = fminf(loB, vB);
+  };
+  const float* p = st + x;
+  f2 pv = bc2(0.0f), cu = row_edge(p), nx = bc2(0.0f);
+  if (H > 1) nx = H > 2 ? row(p + W) : row_edge(p + W);
+  take(div(add2(add2(pv, cu), nx), nce, rce), 0);  // top grid row
+  pv = cu;
+  cu = nx;
+  p += W;
+  int y = 1;
+  for (; y < H - 2; ++y) {  // interior rows whose row below is interior too
+    nx = row(p + W);
+    take(div(add2(add2(pv, cu), nx), nci, rci), y);
+    pv = cu;
+    cu = nx;
+    p += W;
+  }
+  if (y < H - 1) {  // the last interior row: the row below is the bottom grid row
+    nx = row_edge(p + W);
+    take(div(add2(add2(pv, cu), nx), nci, rci), y);
+    pv = cu;
+    cu = nx;
+    ++y;
+  }
+  if (y < H) take(div(add2(pv, cu), nce, rce), y);  // bottom grid row (y = H - 1 > 0)
+  unsigned long long key = key_max(a.key, scan_key(best0, brow0 * W + x));
+  if (liveB) key = key_max(key, scan_key(best1, brow1 * W + x + 1));
+  a.key = key;
+  a.lo = liveB ? fminf(loA, loB) : loA;
+  tame = tame && mx <= 0x49800000u && fr == 0u;
+}
+
+// M of a tame spot (init_count_tame's test, g >= floor(thr) + 1, the threshold clamped the same
+// way) over its N contiguous staged pixels: 16-byte loads strided over the spot's L lanes.  The
+// first and last chunk reach outside the spot (into valid staging memory) and are masked by index
+// (u16: every chunk is counted whole, and the lanes holding those two take back what lies outside).
+template <int L, typename PX>
+__device__ __forceinline__ int count_contig(const PX* sp, int N, double thr, int sl) {
+  double t = floor(thr) + 1.0;
+  t = t < -1.0 ? -1.0 : (t > 2097152.0 ? 2097152.0 : t);
+  constexpr int E = 16 / (int)sizeof(PX);
+  const int h = (int)(((uintptr_t)sp & 15) / sizeof(PX));
+  const uint4* q = reinterpret_cast<const uint4*>(sp - h);
+  const int nc = (h + N + E - 1) / E, tail = nc * E - (h + N);  // h elements before, tail after
+  (void)tail;
+  int m = 0;
+  if constexpr (sizeof(PX) == 4) {
+    // Inner chunks (wholly inside the spot, integer pixels): g >= t <=> sat(g + (1 - t)) = 1, else 0
+    // (every operand an integer below 2^22: exact), summed in f32x2 pairs (exact below 2^24).  The
+    // first and last chunk (partly outside the spot) compare bit patterns under an index mask (tame
+    // f32 pixels are non-negative, so float order is bit-pattern order; t <= 0 counts every one).
+    const float k1 = (float)(1.0 - t);
+    const unsigned tb = __float_as_uint(fmaxf((float)t, 0.0f));
+    f2 s01 = bc2(0.0f), s23 = bc2(0.0f);
+#pragma unroll 2
+    for (int c = sl ? sl : L; c < nc - 1; c += L) {
+      const float4 v = reinterpret_cast<const float4*>(q)[c];
+      s01 = add2(s01, pk2(__saturatef(__fadd_rn(v.x, k1)), __saturatef(__fadd_rn(v.y, k1))));
+      s23 = add2(s23, pk2(__saturatef(__fadd_rn(v.z, k1)), __saturatef(__fadd_rn(v.w, k1))));
+    }
+    float a0, a1, b0, b1;
+    up2(s01, a0, a1);
+    up2(s23, b0, b1);
+    m = (int)((a0 + a1) + (b0 + b1));
+    auto edge = [&](int c) {
+      const uint4 v = q[c];
+      const unsigned u[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) m += (c * 4 + j >= h && c * 4 + j < h + N && u[j] >= tb) ? 1 : 0;
+    };
+    if (sl == 0) edge(0);
+    if (nc > 1 && sl == (nc - 1) % L) edge(nc - 1);
+  } else {
+    const int tt = (int)t;
+    auto ge2 = [&](unsigned w, int j) { return (int)((w >> (16 * (j & 1))) & 0xffffu) >= tt ? 1 : 0; };
+#pragma unroll 2
+    for (int c = sl; c < nc; c += L) {
+      const uint4 v = q[c];
+      const unsigned w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) m += ge2(w[j >> 1], j);
+    }
+    if (sl == 0) {
+      const uint4 v = q[0];
+      const unsigned w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int j = 0; j < 7; ++j) m -= j < h ? ge2(w[j >> 1], j) : 0;
+    }
+    if (sl == (nc - 1) % L) {
+      const uint4 v = q[nc - 1];
+      const unsigned w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int j = 1; j < 8; ++j) m -= j >= 8 - tail ? ge2(w[j >> 1], j) : 0;
+    }
+  }
+  return m;
+}
+
 template <int L, typename PX>
 __global__ void __launch_bounds__(32 * kInitWarps, 3) init_kernel(const PX* __restrict__ images, int W, int H,
                                                               int64_t count, int P, double smin, double smax,
@@ -204,6 +451,10 @@ __global__ void __launch_bounds__(32 * kInitWarps, 3) init_kernel(const PX* __re
   const int64_t ntask = (count + G - 1) / G;
   const int64_t stride = (int64_t)gridDim.x * kInitWarps;
   const uintptr_t lo = (uintptr_t)images, hi = (uintptr_t)(images + count * (int64_t)N);
+  // the warp's two staging mbarriers (after the sigma table)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(
+      init_smem + ((16 + (size_t)kInitWarps * 2 * be * sizeof(PX) + (size_t)(N + 1) * sizeof(float) + 7) & ~(size_t)7)) +
+      2 * warp;
   // stage task t (spots t*G .. t*G+G-1) into buffer b; returns the first spot's element offset
   auto stage = [&](int64_t t, int b) -> int {
     const PX* src = images + t * G * (int64_t)N;
@@ -212,6 +463,26 @@ __global__ void __launch_bounds__(32 * kInitWarps, 3) init_kernel(const PX* __re
     if (e0 > ((hi + 15) & ~(uintptr_t)15)) e0 = (hi + 15) & ~(uintptr_t)15;
     const int nck = (int)((e0 - a0) >> 4);
     PX* dst = buf + b * be;
+#if SF_INIT_TMA
+    if (a0 >= lo && e0 <= hi) {  // the whole window inside the caller's array: one bulk copy
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // after the warp's reads of dst
+        mbar_arrive_tx(&bars[b], (uint32_t)(e0 - a0));
+        bulk_to_smem(dst, reinterpret_cast<const void*>(a0), (uint32_t)(e0 - a0), &bars[b]);
+      }
+      return (int)(((uintptr_t)src & 15) / sizeof(PX));
+    }
+    for (int c = lane; c < nck; c += 32) {  // the window pokes out of the caller's array
+      const uintptr_t cs = a0 + 16 * (uintptr_t)c;
+#pragma unroll
+      for (int w = 0; w < 16 / (int)sizeof(PX); ++w)
+        if (cs + sizeof(PX) * w >= lo && cs + sizeof(PX) * (w + 1) <= hi)
+          reinterpret_cast<PX*>(dst)[(16 / sizeof(PX)) * c + w] = *reinterpret_cast<const PX*>(cs + sizeof(PX) * w);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&bars[b]);
+    return (int)(((uintptr_t)src & 15) / sizeof(PX));
+#else
     if (a0 >= lo && e0 <= hi) {  // the whole window inside the caller's array: 16-byte copies only
       const char* s0 = reinterpret_cast<const char*>(a0);
       float* d0 = reinterpret_cast<float*>(dst);
@@ -232,10 +503,18 @@ __global__ void __launch_bounds__(32 * kInitWarps, 3) init_kernel(const PX* __re
       }
     }
     return (int)(((uintptr_t)src & 15) / sizeof(PX));
+#endif
   };
   // sigma(M) for every possible M, once per CTA (init_sigma: the same f64 ops, so the same floats)
   float* sig_tab = reinterpret_cast<float*>(init_smem + 16 + (size_t)kInitWarps * 2 * be * sizeof(PX));
   for (int m = threadIdx.x; m <= N; m += blockDim.x) sig_tab[m] = init_sigma(m, smin, smax);
+#if SF_INIT_TMA
+  if (lane == 0) {
+    mbar_init(&bars[0]);
+    mbar_init(&bars[1]);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+#endif
   __syncthreads();
   // every 2D grid (W <= 2L): at most two columns per lane, geometry hoisted out of the spot loop
   const bool narrow = W <= 2 * L;
@@ -249,7 +528,9 @@ __global__ void __launch_bounds__(32 * kInitWarps, 3) init_kernel(const PX* __re
   int64_t t = (int64_t)blockIdx.x * kInitWarps + warp;
   int off0 = 0, off1 = 0;  // window offsets of the two staging buffers (registers, no local array)
   if (t < ntask) off0 = stage(t, 0);
+#if !SF_INIT_TMA
   cp_async_commit();
+#endif
 #pragma unroll 1
   for (int i = 0; t < ntask; t += stride, ++i) {
     const int b = i & 1;
@@ -258,8 +539,12 @@ __global__ void __launch_bounds__(32 * kInitWarps, 3) init_kernel(const PX* __re
       if (b) off0 = o;
       else off1 = o;
     }
+#if SF_INIT_TMA
+    mbar_wait(&bars[b], (uint32_t)(i >> 1) & 1u);  // this task's window has landed (use i >> 1 of buffer b)
+#else
     cp_async_commit();
     asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // this task's copies have landed
+#endif
     __syncwarp();
     const int64_t spot = t * G + sub;
     const bool valid = spot < count;
@@ -270,7 +555,16 @@ __global__ void __launch_bounds__(32 * kInitWarps, 3) init_kernel(const PX* __re
     if (narrow) {  // speculative tame walk that checks tameness as it goes
       if (valid && tc0.active) {
         if (two)
+#if SF_INIT_PAIR
+        {
+          if constexpr (sizeof(PX) == 4)
+            walk_pair_f32(reinterpret_cast<const float*>(sp), W, H, tcs, live[1], a, tame);
+          else
+            walk_pair<PX>(sp, W, H, tcs, live[1], a, tame);
+        }
+#else
           walk_tame<2, PX>(sp, W, H, tcs, a, tame);
+#endif
         else
           walk_tame<1, PX>(sp, W, H, one, a, tame);
       }
@@ -299,10 +593,14 @@ __global__ void __launch_bounds__(32 * kInitWarps, 3) init_kernel(const PX* __re
     init_finish(a, idx, alpha, beta, thr);
     int m = 0;
     if (valid) {
+#if SF_INIT_CCOUNT
+      m = tame ? count_contig<L, PX>(sp, N, thr, sl) : init_count(sp, N, thr, sl, L);
+#else
       if (tame && narrow)
         m = !tc0.active ? 0 : (two ? count_columns<2, PX>(sp, W, tcs, live, thr) : count_columns<1, PX>(sp, W, one, live1, thr));
       else
         m = tame ? init_count_tame(sp, N, thr, sl, L) : init_count(sp, N, thr, sl, L);
+#endif
     }
 #pragma unroll
     for (int o = 1; o < L; o <<= 1) m += __shfl_xor_sync(kFull, m, o);
@@ -317,7 +615,9 @@ __global__ void __launch_bounds__(32 * kInitWarps, 3) init_kernel(const PX* __re
     }
     __syncwarp();  // buffer b is restaged two tasks later
   }
+#if !SF_INIT_TMA
   cp_async_wait_all();
+#endif
 }
 
 template <int L, typename PX>
@@ -325,8 +625,9 @@ cudaError_t launch_init_l(const PX* images, int W, int H, int64_t count, int P, 
                           float* inits, float* amps, cudaStream_t stream) {
   constexpr int G = 32 / L;
   // staging buffers (<= 66 KB) + the sigma(M) table
-  const size_t smem = 16 + (size_t)kInitWarps * 2 * init_buf_elems<PX>(G, W * H) * sizeof(PX) +
-                      (size_t)(W * H + 1) * sizeof(float);
+  const size_t smem = ((16 + (size_t)kInitWarps * 2 * init_buf_elems<PX>(G, W * H) * sizeof(PX) +
+                       (size_t)(W * H + 1) * sizeof(float) + 7) & ~(size_t)7) +
+                     (size_t)kInitWarps * 2 * sizeof(uint64_t);
   auto kern = init_kernel<L, PX>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

@@ -297,3 +297,27 @@ def test_tame_division_exhaustive(sf):
     m = torch.zeros(1, dtype=torch.int64, device="cuda")
     sf._lib.check(sf._lib.lib().sf_debug_tame_div_device(m.data_ptr(), torch.cuda.current_stream().cuda_stream))
     assert int(m.item()) == 0
+
+
+def test_standalone_initializer_geometry_sweep(sf):
+    """The standalone initializer (sf_init.cu) on every grid width 1..32 against the vectorised
+    oracle: one column per lane, row-segmented columns (W < L / 2), two adjacent columns per lane
+    (L < W <= 2L) and the general wide path; tame (integer) and general (fractional) spots mixed;
+    odd counts (the last staging window pokes out of the array) and a device batch that starts
+    4 bytes past a 16-byte boundary (every window takes the element-copy path at its edges)."""
+    import torch
+
+    rng = np.random.default_rng(11)
+    for W in range(1, 33):
+        for H in (1, 2, 3, 7, 16, 31, 32):
+            count = 301
+            im = _sim(sf, W, H, count, seed=1000 + 33 * W + H).astype(np.float32)
+            im[rng.random(count) < 0.3] += np.float32(0.5)  # general-path spots
+            grid = sf.PixelGrid(W, H)
+            oi, oa = oinit.estimate_initial_batch_np(im, W, H, 0.3, float(max(W, H)), 3)
+            si, sa = sf.estimate_initial_batch(im, 3, grid=grid)
+            assert bits_equal(si, oi) and bits_equal(sa, oa), (W, H, "host")
+            flat = torch.zeros(count * W * H + 1, dtype=torch.float32, device="cuda")
+            flat[1:] = torch.from_numpy(im.reshape(-1)).cuda()
+            di, da = sf.estimate_initial_batch(flat[1:].view(count, H, W), 3, grid=grid)
+            assert bits_equal(np.asarray(di), oi) and bits_equal(np.asarray(da), oa), (W, H, "offset device")
