@@ -438,6 +438,33 @@ class KernelLeg:
         return {"params": par, "alpha": f[0], "beta": f[1], "nchi2": f[2], "status": u8[0], "iterations": u8[1]}
 
 
+def initializer_leg(sf, dev, d_img, W, H, count, model, reps=10):
+    """The standalone GPU initializer (sf_estimate_initial_device, sf_init.cu) on the headline's
+    HBM-resident batch (> L2), CUDA events on the launching stream.  Not part of `value` (PAPER.md:212
+    times the fit from given inits); it runs in front of the fit for inits=None batches above the
+    fused-initializer size.  Bytes: 4N in + 4P out per spot."""
+    import torch
+
+    grid, cfg, P = sf.PixelGrid(W, H), sf.FitConfig(), min(model, 4) if model != 5 else 3
+    with torch.cuda.device(dev):
+        for _ in range(3):
+            sf.batch_engine.estimate_initial_device(d_img, grid, P, cfg)
+        st = torch.cuda.current_stream(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        e0.record(st)
+        for _ in range(reps):
+            sf.batch_engine.estimate_initial_device(d_img, grid, P, cfg)
+        e1.record(st)
+        torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / reps
+    gbs = count * (4 * W * H + 4 * P) / (ms * 1e-3) / 1e9
+    peak = load_peaks().get("hbm_gbs")
+    return {"ms_per_launch": ms, "spots_per_s": count / (ms * 1e-3), "achieved_GBps": gbs, "peak_GBps": peak,
+            "frac": gbs / peak if peak else None, "launches": reps, "bytes_per_spot": 4 * W * H + 4 * P,
+            "note": "standalone initializer on the headline batch (> L2), untimed by `value`"}
+
+
 def time_legs(legs, steps, warmup, devs, clock=None):
     """Launch every leg `steps` times (all devices concurrently), CUDA events on each launching
     stream; -> (max ms over devices and ranks, per-device ms)."""
@@ -546,6 +573,7 @@ def run_ours(args):
         _, images0, _, d_ini0 = batches[0]
         idx = np.linspace(0, count - 1, min(count, args.parity_sample)).astype(np.int64)
         result["parity"] = parity(legs[0].results(idx), images0[idx], d_ini0.cpu().numpy()[idx], W, H)
+        result["initializer"] = initializer_leg(sf, devs.ids[0], batches[0][2], W, H, count, model)
     del legs
 
     # ---- end to end through the public API from host memory (all devices of this process)
