@@ -321,3 +321,21 @@ def test_standalone_initializer_geometry_sweep(sf):
             flat[1:] = torch.from_numpy(im.reshape(-1)).cuda()
             di, da = sf.estimate_initial_batch(flat[1:].view(count, H, W), 3, grid=grid)
             assert bits_equal(np.asarray(di), oi) and bits_equal(np.asarray(da), oa), (W, H, "offset device")
+
+
+def test_standalone_initializer_u16_geometry_sweep(sf):
+    """The 16-bit instantiation of the standalone initializer (integer column walk, 8-per-chunk M
+    count) on every grid width: device uint16 batches above the fused-initializer size without
+    inits run it in front of the fit; the results equal the float32 batch's (whose initializer the
+    f32 sweep pins to the oracle) bit for bit."""
+    import torch
+
+    count = 16_400  # > sf_launch.h:kFusedInitMaxSpots
+    for W in range(1, 33):
+        for H in (3, 16, 32):
+            grid = sf.PixelGrid(W, H)
+            d, _ = sf.simulate_batch_device(sf.SimConfig(width=W, height=H, count=count, seed=7 * W + H))
+            d = d.reshape(count, W * H)
+            a = sf.fit_batch(d, grid=grid)
+            b = sf.fit_batch(torch.from_numpy(d.cpu().numpy().astype(np.uint16)).cuda(), grid=grid)
+            _same(b, a, f"u16 device {W}x{H}")
