@@ -21,7 +21,13 @@ namespace {
 // per-spot reductions are shared by G spots per instruction.  A tame spot (every
 // pixel an integer in [0, 2^20]: camera counts) takes the exact integer column
 // walk of sf_init_core.cuh; any other spot the general f64 scan.
-constexpr int kInitWarps = 8;
+#ifndef SF_INIT_WARPS
+#define SF_INIT_WARPS 8
+#endif
+#ifndef SF_INIT_MINB
+#define SF_INIT_MINB 3
+#endif
+constexpr int kInitWarps = SF_INIT_WARPS;
 
 #ifndef SF_INIT_PAIR
 #define SF_INIT_PAIR 1  // L < W <= 2L: a lane walks two adjacent columns off one set of row loads
@@ -435,7 +441,7 @@ __device__ __forceinline__ int count_contig(const PX* sp, int N, double thr, int
 }
 
 template <int L, typename PX>
-__global__ void __launch_bounds__(32 * kInitWarps, 3) init_kernel(const PX* __restrict__ images, int W, int H,
+__global__ void __launch_bounds__(32 * kInitWarps, SF_INIT_MINB) init_kernel(const PX* __restrict__ images, int W, int H,
                                                               int64_t count, int P, double smin, double smax,
                                                               float* __restrict__ inits, float* __restrict__ amps) {
   constexpr int G = 32 / L;
