@@ -28,6 +28,25 @@ namespace {
 #define SF_INIT_MINB 3
 #endif
 constexpr int kInitWarps = SF_INIT_WARPS;
+#ifndef SF_INIT_QUAD
+#define SF_INIT_QUAD 1  // 8 < W <= 16 (f32): four adjacent columns per lane, 4 lanes and 8 spots per warp
+#endif
+#ifndef SF_INIT_WARPS4
+#define SF_INIT_WARPS4 3
+#endif
+#ifndef SF_INIT_MINB4
+#define SF_INIT_MINB4 5
+#endif
+// warps per CTA and launch-bound CTAs per SM: the quad walk (L = 4) stages 8 spots per warp, so it
+// runs fewer warps per CTA to keep three CTAs of staging per SM
+template <int L>
+__host__ __device__ constexpr int init_warps() {
+  return L == 4 ? SF_INIT_WARPS4 : kInitWarps;
+}
+template <int L>
+__host__ __device__ constexpr int init_minb() {
+  return L == 4 ? SF_INIT_MINB4 : SF_INIT_MINB;
+}
 
 #ifndef SF_INIT_PAIR
 #define SF_INIT_PAIR 1  // L < W <= 2L: a lane walks two adjacent columns off one set of row loads
@@ -374,6 +393,101 @@ __device__ __forceinline__ void walk_pair_f32(const float* st, int W, int H, con
   tame = tame && mx <= 0x49800000u && fr == 0u;
 }
 
+// The tame walk of four adjacent columns x .. x + 3 of one lane (8 < W <= 16, L = 4), the columns in
+// the halves of two f32x2 registers: a row's six loads r[-1 .. 4] give all four horizontal 3-sums,
+// otherwise walk_pair_f32's arithmetic and edge handling (a missing neighbour or a column beyond the
+// grid reads a pixel of the row itself in the top and bottom grid rows, a pixel of the same spot
+// elsewhere, and is multiplied by 0 or dropped from the scan).
+__device__ __forceinline__ void walk_quad_f32(const float* st, int W, int H, int x, InitScan& a, bool& tame) {
+  bool live[4];
+  float cif[4], cef[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    live[k] = x + k < W;
+    const int xc = live[k] ? x + k : x;
+    const int cxi = 1 + (xc > 0) + (xc < W - 1);
+    cif[k] = (float)(3 * cxi);
+    cef[k] = (float)((H > 1 ? 2 : 1) * cxi);
+  }
+  const f2 nciA = pk2(-cif[0], -cif[1]), nciB = pk2(-cif[2], -cif[3]);
+  const f2 rciA = pk2(__frcp_rn(cif[0]), __frcp_rn(cif[1])), rciB = pk2(__frcp_rn(cif[2]), __frcp_rn(cif[3]));
+  const f2 nceA = pk2(-cef[0], -cef[1]), nceB = pk2(-cef[2], -cef[3]);
+  const f2 rceA = pk2(__frcp_rn(cef[0]), __frcp_rn(cef[1])), rceB = pk2(__frcp_rn(cef[2]), __frcp_rn(cef[3]));
+  const int oL = x > 0 ? -1 : 0, o1 = live[1] ? 1 : 0, o2 = live[2] ? 2 : 0, o3 = live[3] ? 3 : 0,
+            o4 = x + 4 < W ? 4 : 0;
+  const f2 mLa = pk2(x > 0 ? 1.0f : 0.0f, 1.0f);
+  const f2 mRa = pk2(live[1] ? 1.0f : 0.0f, live[2] ? 1.0f : 0.0f);
+  const f2 mRb = pk2(live[3] ? 1.0f : 0.0f, x + 4 < W ? 1.0f : 0.0f);
+  const f2 big = bc2(8388608.0f), nbig = bc2(-8388608.0f), nz = bc2(-0.0f);
+  unsigned mx = 0u, fr = 0u;
+  float lo0 = a.lo, lo1 = a.lo, lo2 = a.lo, lo3 = a.lo;
+  float b0 = -1.0f, b1 = -1.0f, b2 = -1.0f, b3 = -1.0f;
+  int y0r = 0, y1r = 0, y2r = 0, y3r = 0;
+  auto hsum = [&](float l, float r0, float r1, float r2, float r3, float r4, f2& hA, f2& hB) {
+    mx = __vimax3_u32(mx, __float_as_uint(r0), __float_as_uint(r1));
+    mx = __vimax3_u32(mx, __float_as_uint(r2), __float_as_uint(r3));
+    const f2 cA = pk2(r0, r1), cB = pk2(r2, r3);
+    const f2 iA = add2(add2(cA, big), nbig), iB = add2(add2(cB, big), nbig);  // tame check per half
+    const unsigned long long d = (iA.v ^ cA.v) | (iB.v ^ cB.v);
+    fr |= (unsigned)d | (unsigned)(d >> 32);
+    const f2 p12 = pk2(r1, r2);
+    hA = fma2(p12, mRa, fma2(pk2(l, r0), mLa, cA));  // (r0 + l [x > 0] + r1 [.], r1 + r0 + r2 [.])
+    hB = fma2(pk2(r3, r4), mRb, add2(p12, cB));      // (r2 + r1 + r3 [.], r3 + r2 + r4 [.])
+  };
+  auto row_edge = [&](const float* r, f2& hA, f2& hB) { hsum(r[oL], r[0], r[o1], r[o2], r[o3], r[o4], hA, hB); };
+  auto row = [&](const float* r, f2& hA, f2& hB) { hsum(r[-1], r[0], r[1], r[2], r[3], r[4], hA, hB); };
+  auto div = [&](f2 sum, f2 nc, f2 rc) -> f2 {  // tame_div per half
+    const f2 q0 = mul2(sum, rc, nz);
+    return fma2(fma2(q0, nc, sum), rc, q0);
+  };
+  auto take = [&](f2 vA, f2 vB, int y) {
+    float v0, v1, v2, v3;
+    up2(vA, v0, v1);
+    up2(vB, v2, v3);
+    if (v0 > b0) { b0 = v0; y0r = y; }
+    if (v1 > b1) { b1 = v1; y1r = y; }
+    if (v2 > b2) { b2 = v2; y2r = y; }
+    if (v3 > b3) { b3 = v3; y3r = y; }
+    lo0 = fminf(lo0, v0);
+    lo1 = fminf(lo1, v1);
+    lo2 = fminf(lo2, v2);
+    lo3 = fminf(lo3, v3);
+  };
+  const float* p = st + x;
+  const f2 z = bc2(0.0f);
+  f2 pA = z, pB = z, cA, cB, nA = z, nB = z;
+  row_edge(p, cA, cB);
+  if (H > 1) {
+    if (H > 2) row(p + W, nA, nB);
+    else row_edge(p + W, nA, nB);
+  }
+  take(div(add2(add2(pA, cA), nA), nceA, rceA), div(add2(add2(pB, cB), nB), nceB, rceB), 0);  // top grid row
+  pA = cA; pB = cB; cA = nA; cB = nB;
+  p += W;
+  int y = 1;
+  for (; y < H - 2; ++y) {  // interior rows whose row below is interior too
+    row(p + W, nA, nB);
+    take(div(add2(add2(pA, cA), nA), nciA, rciA), div(add2(add2(pB, cB), nB), nciB, rciB), y);
+    pA = cA; pB = cB; cA = nA; cB = nB;
+    p += W;
+  }
+  if (y < H - 1) {  // the last interior row: the row below is the bottom grid row
+    row_edge(p + W, nA, nB);
+    take(div(add2(add2(pA, cA), nA), nciA, rciA), div(add2(add2(pB, cB), nB), nciB, rciB), y);
+    pA = cA; pB = cB; cA = nA; cB = nB;
+    ++y;
+  }
+  if (y < H) take(div(add2(pA, cA), nceA, rceA), div(add2(pB, cB), nceB, rceB), y);  // bottom grid row
+  unsigned long long key = key_max(a.key, scan_key(b0, y0r * W + x));
+  float lo = lo0;
+  if (live[1]) { key = key_max(key, scan_key(b1, y1r * W + x + 1)); lo = fminf(lo, lo1); }
+  if (live[2]) { key = key_max(key, scan_key(b2, y2r * W + x + 2)); lo = fminf(lo, lo2); }
+  if (live[3]) { key = key_max(key, scan_key(b3, y3r * W + x + 3)); lo = fminf(lo, lo3); }
+  a.key = key;
+  a.lo = lo;
+  tame = tame && mx <= 0x49800000u && fr == 0u;
+}
+
 // M of a tame spot (init_count_tame's test, g >= floor(thr) + 1, the threshold clamped the same
 // way) over its N contiguous staged pixels: 16-byte loads strided over the spot's L lanes.  The
 // first and last chunk reach outside the spot (into valid staging memory) and are masked by index
@@ -441,10 +555,11 @@ __device__ __forceinline__ int count_contig(const PX* sp, int N, double thr, int
 }
 
 template <int L, typename PX>
-__global__ void __launch_bounds__(32 * kInitWarps, SF_INIT_MINB) init_kernel(const PX* __restrict__ images, int W, int H,
+__global__ void __launch_bounds__(32 * init_warps<L>(), init_minb<L>()) init_kernel(const PX* __restrict__ images, int W, int H,
                                                               int64_t count, int P, double smin, double smax,
                                                               float* __restrict__ inits, float* __restrict__ amps) {
   constexpr int G = 32 / L;
+  constexpr int kInitWarps = init_warps<L>();  // (shadows the default for this instantiation)
   extern __shared__ __align__(16) unsigned char init_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int sub = lane / L, sl = lane % L;  // spot of the warp's G, lane within the spot
@@ -558,7 +673,9 @@ __global__ void __launch_bounds__(32 * kInitWarps, SF_INIT_MINB) init_kernel(con
     InitScan a;
     scan_reset(a);
     bool tame = true;
-    if (narrow) {  // speculative tame walk that checks tameness as it goes
+    if constexpr (L == 4) {  // 8 < W <= 16: four adjacent columns per lane
+      if (valid && 4 * sl < W) walk_quad_f32(reinterpret_cast<const float*>(sp), W, H, 4 * sl, a, tame);
+    } else if (narrow) {  // speculative tame walk that checks tameness as it goes
       if (valid && tc0.active) {
         if (two)
 #if SF_INIT_PAIR
@@ -588,7 +705,7 @@ __global__ void __launch_bounds__(32 * kInitWarps, SF_INIT_MINB) init_kernel(con
       if (!tame) {  // the general f64 scan (rare: non-integer or large pixel values)
         scan_reset(a);
         init_scan(sp, W, H, N, invW, sl, L, a);
-      } else if (!narrow) {
+      } else if (!narrow && L != 4) {
         init_scan_tame<L, PX>(sp, W, H, sl, a);
       }
     }
@@ -612,11 +729,14 @@ __global__ void __launch_bounds__(32 * kInitWarps, SF_INIT_MINB) init_kernel(con
     for (int o = 1; o < L; o <<= 1) m += __shfl_xor_sync(kFull, m, o);
     if (valid) {
       const float sg = sig_tab[m];
-      if (sl < P) {  // (x, y, sigma[, sigma]); P = 5 (explicit-5, internal): (x, y, sigma, alpha, beta)
-        const int y = (int)(((float)idx + 0.5f) * invW);  // idx / W exactly (see init_smoothed)
+      // (x, y, sigma[, sigma]); P = 5 (explicit-5, internal): (x, y, sigma, alpha, beta), the fifth
+      // entry by lane 0 when the spot has only 4 lanes
+      const int y = (int)(((float)idx + 0.5f) * invW);  // idx / W exactly (see init_smoothed)
+      if (sl < P)
         inits[spot * P + sl] = sl == 0 ? (float)(idx - y * W)
                                        : (sl == 1 ? (float)y : (sl == 2 || P == 4 ? sg : (sl == 3 ? alpha : beta)));
-      }
+      if constexpr (L < 5)
+        if (P == 5 && sl == 0) inits[spot * P + 4] = beta;
       if (amps != nullptr && sl < 2) amps[2 * spot + sl] = sl == 0 ? alpha : beta;
     }
     __syncwarp();  // buffer b is restaged two tasks later
@@ -630,6 +750,7 @@ template <int L, typename PX>
 cudaError_t launch_init_l(const PX* images, int W, int H, int64_t count, int P, double smin, double smax,
                           float* inits, float* amps, cudaStream_t stream) {
   constexpr int G = 32 / L;
+  constexpr int kInitWarps = init_warps<L>();
   // staging buffers (<= 66 KB) + the sigma(M) table
   const size_t smem = ((16 + (size_t)kInitWarps * 2 * init_buf_elems<PX>(G, W * H) * sizeof(PX) +
                        (size_t)(W * H + 1) * sizeof(float) + 7) & ~(size_t)7) +
@@ -658,6 +779,11 @@ cudaError_t launch_init_px(const PX* images, int W, int H, int64_t count, int P,
   // L lanes per spot, G = 32 / L spots per warp: the fewest lanes that leave each lane at most two
   // columns (W <= 2L) with G * N <= 1024 pixels per warp buffer; more spots per warp share the
   // per-spot reductions and bookkeeping
+  if constexpr (sizeof(PX) == 4 && SF_INIT_QUAD)
+    // odd N only: the 8 spots of a warp start an odd number of words apart, which spreads their
+    // lanes' shared loads over the banks (an even N such as 16x16 lines them up: 8-way conflicts)
+    if (W > 8 && W <= 16 && N <= 256 && (N & 1))
+      return launch_init_l<4, PX>(images, W, H, count, P, sigma_min, sigma_max, inits, amps, stream);
   if (W <= 16 && N <= 256) return launch_init_l<8, PX>(images, W, H, count, P, sigma_min, sigma_max, inits, amps, stream);
   if (W <= 32 && N <= 512) return launch_init_l<16, PX>(images, W, H, count, P, sigma_min, sigma_max, inits, amps, stream);
   return launch_init_l<32, PX>(images, W, H, count, P, sigma_min, sigma_max, inits, amps, stream);
