@@ -87,14 +87,6 @@ int sm_count_of_current() {
   return sms > 0 ? sms : 1;
 }
 
-void shape_need(const sf::Geom& g, int* ch, int* tl) {
-  *ch = 0;
-  *tl = 0;
-  for (int l = 0; l < g.lanes; ++l) {
-    *ch = std::max(*ch, (int)g.nc[l]);
-    *tl = std::max(*tl, (int)g.nt[l]);
-  }
-}
 
 // Work-claim counter slots (sf_fit_kernel.cuh:g_work), per device.  An ordinary
 // launch takes a stream slot whose previous launch has completed (the event

@@ -143,11 +143,11 @@ template <int NC, typename PX>
 __device__ __forceinline__ void walk_tame(const PX* st, int W, int H, const TameCol (&cs)[NC], InitScan& a,
                                           bool& tame) {
   using Acc = typename TameAcc<PX>::T;
-  bool hl[NC], hr[NC];
+  bool hl[NC] = {}, hr[NC] = {};
   const PX* p[NC];
   Acc prev[NC], cur[NC];
-  float best[NC];
-  int brow[NC];
+  float best[NC] = {};
+  int brow[NC] = {};
   unsigned mx = 0u;   // max pixel bit pattern (negative, -0, inf, NaN and > 2^20 all exceed 0x49800000)
   bool frac = false;  // some pixel is not an integer
   float lo = a.lo;
@@ -645,7 +645,9 @@ __global__ void __launch_bounds__(32 * init_warps<L>(), init_minb<L>()) init_ker
   const bool live[2] = {tc0.active, tcs[1].active};
   if (!tcs[1].active) tcs[1] = tc0;  // a lane without a second column repeats its first (same values)
   const TameCol one[1] = {tc0};
+#if !SF_INIT_CCOUNT
   const bool live1[1] = {true};
+#endif
   int64_t t = (int64_t)blockIdx.x * kInitWarps + warp;
   int off0 = 0, off1 = 0;  // window offsets of the two staging buffers (registers, no local array)
   if (t < ntask) off0 = stage(t, 0);
