@@ -29,7 +29,7 @@ namespace {
 #endif
 constexpr int kInitWarps = SF_INIT_WARPS;
 #ifndef SF_INIT_QUAD
-#define SF_INIT_QUAD 1  // 8 < W <= 16 (f32): four adjacent columns per lane, 4 lanes and 8 spots per warp
+#define SF_INIT_QUAD 1  // odd-N f32 grids of width 9..32: four adjacent columns per lane
 #endif
 #ifndef SF_INIT_WARPS4
 #define SF_INIT_WARPS4 3
@@ -37,15 +37,15 @@ constexpr int kInitWarps = SF_INIT_WARPS;
 #ifndef SF_INIT_MINB4
 #define SF_INIT_MINB4 5
 #endif
-// warps per CTA and launch-bound CTAs per SM: the quad walk (L = 4) stages 8 spots per warp, so it
-// runs fewer warps per CTA to keep three CTAs of staging per SM
-template <int L>
+// warps per CTA and launch-bound CTAs per SM: the quad walk stages 7-8 KB of spots per warp and
+// buffer, so it runs fewer warps per CTA
+template <bool QUAD>
 __host__ __device__ constexpr int init_warps() {
-  return L == 4 ? SF_INIT_WARPS4 : kInitWarps;
+  return QUAD ? SF_INIT_WARPS4 : kInitWarps;
 }
-template <int L>
+template <bool QUAD>
 __host__ __device__ constexpr int init_minb() {
-  return L == 4 ? SF_INIT_MINB4 : SF_INIT_MINB;
+  return QUAD ? SF_INIT_MINB4 : SF_INIT_MINB;
 }
 
 #ifndef SF_INIT_PAIR
@@ -554,12 +554,12 @@ __device__ __forceinline__ int count_contig(const PX* sp, int N, double thr, int
   return m;
 }
 
-template <int L, typename PX>
-__global__ void __launch_bounds__(32 * init_warps<L>(), init_minb<L>()) init_kernel(const PX* __restrict__ images, int W, int H,
+template <int L, typename PX, bool QUAD>
+__global__ void __launch_bounds__(32 * init_warps<QUAD>(), init_minb<QUAD>()) init_kernel(const PX* __restrict__ images, int W, int H,
                                                               int64_t count, int P, double smin, double smax,
                                                               float* __restrict__ inits, float* __restrict__ amps) {
   constexpr int G = 32 / L;
-  constexpr int kInitWarps = init_warps<L>();  // (shadows the default for this instantiation)
+  constexpr int kInitWarps = init_warps<QUAD>();  // (shadows the default for this instantiation)
   extern __shared__ __align__(16) unsigned char init_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int sub = lane / L, sl = lane % L;  // spot of the warp's G, lane within the spot
@@ -675,7 +675,7 @@ __global__ void __launch_bounds__(32 * init_warps<L>(), init_minb<L>()) init_ker
     InitScan a;
     scan_reset(a);
     bool tame = true;
-    if constexpr (L == 4) {  // 8 < W <= 16: four adjacent columns per lane
+    if constexpr (QUAD) {  // 4 (L - 1) < W <= 4 L: four adjacent columns per lane
       if (valid && 4 * sl < W) walk_quad_f32(reinterpret_cast<const float*>(sp), W, H, 4 * sl, a, tame);
     } else if (narrow) {  // speculative tame walk that checks tameness as it goes
       if (valid && tc0.active) {
@@ -707,7 +707,7 @@ __global__ void __launch_bounds__(32 * init_warps<L>(), init_minb<L>()) init_ker
       if (!tame) {  // the general f64 scan (rare: non-integer or large pixel values)
         scan_reset(a);
         init_scan(sp, W, H, N, invW, sl, L, a);
-      } else if (!narrow && L != 4) {
+      } else if (!narrow && !QUAD) {
         init_scan_tame<L, PX>(sp, W, H, sl, a);
       }
     }
@@ -748,16 +748,16 @@ __global__ void __launch_bounds__(32 * init_warps<L>(), init_minb<L>()) init_ker
 #endif
 }
 
-template <int L, typename PX>
+template <int L, typename PX, bool QUAD = false>
 cudaError_t launch_init_l(const PX* images, int W, int H, int64_t count, int P, double smin, double smax,
                           float* inits, float* amps, cudaStream_t stream) {
   constexpr int G = 32 / L;
-  constexpr int kInitWarps = init_warps<L>();
+  constexpr int kInitWarps = init_warps<QUAD>();
   // staging buffers (<= 66 KB) + the sigma(M) table
   const size_t smem = ((16 + (size_t)kInitWarps * 2 * init_buf_elems<PX>(G, W * H) * sizeof(PX) +
                        (size_t)(W * H + 1) * sizeof(float) + 7) & ~(size_t)7) +
                      (size_t)kInitWarps * 2 * sizeof(uint64_t);
-  auto kern = init_kernel<L, PX>;
+  auto kern = init_kernel<L, PX, QUAD>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, per_sm = 0;
@@ -784,8 +784,12 @@ cudaError_t launch_init_px(const PX* images, int W, int H, int64_t count, int P,
   if constexpr (sizeof(PX) == 4 && SF_INIT_QUAD)
     // odd N only: the 8 spots of a warp start an odd number of words apart, which spreads their
     // lanes' shared loads over the banks (an even N such as 16x16 lines them up: 8-way conflicts)
-    if (W > 8 && W <= 16 && N <= 256 && (N & 1))
-      return launch_init_l<4, PX>(images, W, H, count, P, sigma_min, sigma_max, inits, amps, stream);
+    if (N & 1) {
+      if (W > 8 && W <= 16 && N <= 256)
+        return launch_init_l<4, PX, true>(images, W, H, count, P, sigma_min, sigma_max, inits, amps, stream);
+      if (W > 16 && W <= 32 && N <= 512)
+        return launch_init_l<8, PX, true>(images, W, H, count, P, sigma_min, sigma_max, inits, amps, stream);
+    }
   if (W <= 16 && N <= 256) return launch_init_l<8, PX>(images, W, H, count, P, sigma_min, sigma_max, inits, amps, stream);
   if (W <= 32 && N <= 512) return launch_init_l<16, PX>(images, W, H, count, P, sigma_min, sigma_max, inits, amps, stream);
   return launch_init_l<32, PX>(images, W, H, count, P, sigma_min, sigma_max, inits, amps, stream);
