@@ -766,11 +766,13 @@ def per_config(sf, args, dev):
         images = d_img.index_select(0, ti).cpu().numpy()
         inits = d_ini.index_select(0, ti).cpu().numpy()
         par = parity(leg.results(idx), images, inits, W, H)
+        ini_leg = initializer_leg(sf, dev, d_img, W, H, count, model, reps=5 if count > 1_000_000 else 10)
         out[name] = {"workload": f"{count} {MODEL_NAME[model]} spots, {W}x{H} px", "spots": count,
                      "value": count * steps / (ms * 1e-3), "unit": "fits/s", "ms_per_step": ms / steps,
                      "steps": steps, "roofline_frac": rf["frac"], "ops_per_fit": rf["ops_per_fit"],
                      "evals_per_fit": rf["evals_per_fit"], "parity": par, "setup_s": setup,
-                     "input_bytes": count * W * H * 4}
+                     "input_bytes": count * W * H * 4,
+                     "initializer": {k: ini_leg[k] for k in ("ms_per_launch", "achieved_GBps", "frac")}}
         del leg, d_img, d_ini
         torch.cuda.empty_cache()
     return out
