@@ -82,7 +82,7 @@ def build(force: bool = False, jobs: int = 0, verbose: bool = False, variant: st
     src = os.path.join(CSRC, "sf_host_narrow.cpp")
     out = os.path.join(obj, "sf_host_narrow.o")
     tasks.append((out, [src, os.path.join(INCLUDE, "spotfit.h"), __file__],
-                  ["g++", "-O3", "-fPIC", "-std=c++17", "-pthread", f"-I{INCLUDE}", "-c", src, "-o", out]))
+                  ["g++", "-O3", "-fPIC", "-std=c++17", "-pthread", f"-I{INCLUDE}"] + dflags + ["-c", src, "-o", out]))
     src = os.path.join(CSRC, "sf_csv.cpp")
     out = os.path.join(obj, "sf_csv_host.o")
     tasks.append((out, [src, os.path.join(CSRC, "sf_pow5_tables.h"), os.path.join(INCLUDE, "spotfit.h"), __file__],

@@ -356,23 +356,8 @@ struct HostJob {
 
 // Pageable host input is staged into pinned buffers by the CPU.  One thread copies ~10 GB/s, far
 // below PCIe (~53 GB/s), so large chunks are copied by copy_threads threads (the host's cores split
-// over the devices of the call; SPOTFIT_COPY_THREADS overrides).
-void par_memcpy(void* dst, const void* src, size_t bytes, int threads) {
-  constexpr size_t kPiece = 4u << 20;
-  const int T = (int)std::min<size_t>((size_t)std::max(1, threads), (bytes + kPiece - 1) / kPiece);
-  if (T <= 1) {
-    std::memcpy(dst, src, bytes);
-    return;
-  }
-  const size_t per = ((bytes + T - 1) / T + 63) & ~(size_t)63;
-  std::vector<std::thread> th;
-  for (int t = 1; t < T; ++t) {
-    const size_t a = std::min(bytes, per * t), b = std::min(bytes, per * (t + 1));
-    if (b > a) th.emplace_back([=] { std::memcpy((char*)dst + a, (const char*)src + a, b - a); });
-  }
-  std::memcpy(dst, src, std::min(bytes, per));
-  for (auto& x : th) x.join();
-}
+// over the devices of the call; SPOTFIT_COPY_THREADS overrides): sf::par_copy.
+void par_memcpy(void* dst, const void* src, size_t bytes, int threads) { sf::par_copy(dst, src, bytes, threads); }
 
 void copy_out_staged(Slot& s, HostJob& j) {
   if (!s.pending) return;

@@ -38,9 +38,16 @@ bool narrow_scalar(uint16_t* dst, const float* src, size_t n) {
   return ok;
 }
 
+#ifndef SF_HOST_NT
+#define SF_HOST_NT 1  // streaming (non-temporal) stores into the pinned staging buffers
+#endif
+
 __attribute__((target("avx2"))) bool narrow_avx2(uint16_t* dst, const float* src, size_t n) {
   const __m256i lim = _mm256_set1_epi32(0x477FFF00);
   __m256i bad = _mm256_setzero_si256();
+  // A 32-byte aligned destination (the pinned staging buffer) takes streaming stores: the lines go
+  // to memory for the DMA without being read first
+  const bool nt = SF_HOST_NT && ((uintptr_t)dst & 31) == 0;
   size_t i = 0;
   for (; i + 16 <= n; i += 16) {
     const __m256 v0 = _mm256_loadu_ps(src + i), v1 = _mm256_loadu_ps(src + i + 8);
@@ -55,8 +62,12 @@ __attribute__((target("avx2"))) bool narrow_avx2(uint16_t* dst, const float* src
                                                _mm256_or_si256(_mm256_castps_si256(e0), _mm256_castps_si256(e1))));
     // pack to u16 (per 128-bit lane), then restore element order
     const __m256i p = _mm256_permute4x64_epi64(_mm256_packus_epi32(i0, i1), 0xD8);
-    _mm256_storeu_si256(reinterpret_cast<__m256i*>(dst + i), p);
+    if (nt)
+      _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i), p);
+    else
+      _mm256_storeu_si256(reinterpret_cast<__m256i*>(dst + i), p);
   }
+  if (nt) _mm_sfence();
   bool ok = _mm256_testz_si256(bad, bad) != 0;
   for (; i < n; ++i) ok &= narrow_one(src[i], dst[i]);
   return ok;
@@ -67,9 +78,54 @@ bool narrow_block(uint16_t* dst, const float* src, size_t n) {
   return avx2 ? narrow_avx2(dst, src, n) : narrow_scalar(dst, src, n);
 }
 
+// memcpy into a 32-byte aligned destination with streaming stores (the source unaligned)
+__attribute__((target("avx2"))) void copy_nt_avx2(void* dst, const void* src, size_t bytes) {
+  char* d = static_cast<char*>(dst);
+  const char* s = static_cast<const char*>(src);
+  size_t i = 0;
+  for (; i + 128 <= bytes; i += 128) {
+    const __m256i a = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(s + i));
+    const __m256i b = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(s + i + 32));
+    const __m256i c = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(s + i + 64));
+    const __m256i e = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(s + i + 96));
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(d + i), a);
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(d + i + 32), b);
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(d + i + 64), c);
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(d + i + 96), e);
+  }
+  _mm_sfence();
+  if (i < bytes) memcpy(d + i, s + i, bytes - i);
+}
+
+void copy_block(void* dst, const void* src, size_t bytes) {
+  static const bool avx2 = __builtin_cpu_supports("avx2");
+  if (SF_HOST_NT && avx2 && ((uintptr_t)dst & 31) == 0 && bytes >= 4096)
+    copy_nt_avx2(dst, src, bytes);
+  else
+    memcpy(dst, src, bytes);
+}
+
 }  // namespace
 
 namespace sf {
+
+// memcpy over `threads` threads (pinned staging of pageable input), streaming stores when possible
+void par_copy(void* dst, const void* src, size_t bytes, int threads) {
+  constexpr size_t kPiece = 4u << 20;
+  const int T = (int)std::min<size_t>((size_t)std::max(1, threads), (bytes + kPiece - 1) / kPiece);
+  if (T <= 1) {
+    copy_block(dst, src, bytes);
+    return;
+  }
+  const size_t per = ((bytes + T - 1) / T + 63) & ~(size_t)63;
+  std::vector<std::thread> th;
+  for (int t = 1; t < T; ++t) {
+    const size_t a = std::min(bytes, per * t), b = std::min(bytes, per * (t + 1));
+    if (b > a) th.emplace_back([=] { copy_block((char*)dst + a, (const char*)src + a, b - a); });
+  }
+  copy_block(dst, src, std::min(bytes, per));
+  for (auto& x : th) x.join();
+}
 
 // dst[i] = (uint16_t)src[i] for i < n over `threads` threads; true iff every value narrowed exactly
 bool par_narrow_u16(uint16_t* dst, const float* src, size_t n, int threads) {

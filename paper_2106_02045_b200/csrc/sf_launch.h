@@ -82,6 +82,8 @@ cudaError_t launch_model_chi_gradient(const float* g, const float* f, const floa
 // lossless f32 -> u16 narrowing of a host chunk for the PCIe leg (sf_host_narrow.cpp): true iff every
 // value is an integer in [0, 65535] with a clear sign bit
 bool par_narrow_u16(uint16_t* dst, const float* src, size_t n, int threads);
+// memcpy over `threads` threads, streaming stores into an aligned destination (sf_host_narrow.cpp)
+void par_copy(void* dst, const void* src, size_t bytes, int threads);
 
 // device simulator (sf_sim.cu)
 cudaError_t launch_simulate(const sf_sim_config& c, int W, int H, int64_t first, int64_t count, float* images,
