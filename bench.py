@@ -706,24 +706,29 @@ def e2e_legs(sf, args, devs, batches, W, H, count, model):
             s += devs.max(time.perf_counter() - a)
         return devs.n_gpus * count * steps / s, r
 
+    def h2d(r):  # bytes the library actually copied host -> device in one call (sf_stats.h2d_bytes)
+        return int(r.stats.get("h2d_bytes") or 0)
+
     v_fused, r = timed(lambda: sf.fit_batch(pin_img, None, out=outs, **call))
-    res = {"e2e": {"value": v_fused, "unit": "fits/s", "h2d_bytes_per_step": total * npx * 4,
-                   "d2h_bytes_per_step": d2h, "steps": steps, "chunks_per_step": r.stats.get("n_chunks"),
-                   "path": "fit_batch(pinned images) -> sf_fit_batch, inits=None: the fit kernel's fused initializer "
-                           "(no separate init pass, pixels cross PCIe once), chunked H2D/kernel/D2H on "
+    res = {"e2e": {"value": v_fused, "unit": "fits/s", "h2d_bytes_per_step": h2d(r), "d2h_bytes_per_step": d2h,
+                   "input_bytes_per_step": total * npx * 4, "steps": steps,
+                   "chunks_per_step": r.stats.get("n_chunks"), "chunks_u16_per_step": r.stats.get("n_chunks_u16"),
+                   "path": "fit_batch(pinned f32 images) -> sf_fit_batch, inits=None: integer-valued chunks narrowed "
+                           "losslessly to u16 by the host (half the PCIe bytes; h2d_bytes_per_step counts what "
+                           "crossed), initializer on the device, chunked H2D/kernel/D2H on "
                            f"{nd} device(s) of this process"}}
     keep = min(total, 50_000)
     fused = {k: np.array(getattr(outs, k)[:keep]) for k in FIELDS}
-    v_in, _ = timed(lambda: sf.fit_batch(pin_img, pin_ini, out=outs, **call))
+    v_in, r_in = timed(lambda: sf.fit_batch(pin_img, pin_ini, out=outs, **call))
     same = all(np.array_equal(fused[k].view(np.uint8), np.asarray(getattr(outs, k)[:keep]).view(np.uint8))
                for k in FIELDS)
     variants = {"pinned_with_inits": {"value": v_in, "unit": "fits/s",
-                                      "h2d_bytes_per_step": total * (npx * 4 + 4 * model), "d2h_bytes_per_step": d2h,
+                                      "h2d_bytes_per_step": h2d(r_in), "d2h_bytes_per_step": d2h,
                                       "path": "fit_batch(pinned images, pinned inits, out=pinned): the paper's span "
                                               "(PAPER.md:210, init excluded)"},
                 "fused_equals_explicit_inits": {"spots": keep, "bitwise": bool(same)}}
-    v_pg, _ = timed(lambda: sf.fit_batch(images, None, **call))
-    variants["pageable_no_inits"] = {"value": v_pg, "unit": "fits/s", "h2d_bytes_per_step": total * npx * 4,
+    v_pg, r_pg = timed(lambda: sf.fit_batch(images, None, **call))
+    variants["pageable_no_inits"] = {"value": v_pg, "unit": "fits/s", "h2d_bytes_per_step": h2d(r_pg),
                                      "d2h_bytes_per_step": d2h,
                                      "path": "fit_batch(numpy images): pageable in, new result arrays out, fused "
                                              "initializer (the plain drop-in call)"}
@@ -734,6 +739,16 @@ def e2e_legs(sf, args, devs, batches, W, H, count, model):
             "value": v16, "unit": "fits/s", "h2d_bytes_per_step": total * npx * 2, "d2h_bytes_per_step": d2h,
             "path": "fit_batch(pinned uint16 counts) -> sf_fit_batch_u16 (half the PCIe bytes; staged as u16 and "
                     "widened in the fit kernel), fused initializer"}
+    # the same call on pixels that do not narrow (every value + 0.5): f32 crosses PCIe, after the first
+    # chunk's narrowing pass gives up at its first value
+    frac_img = pin_img  # reuse the pinned buffer: +0.5 in place, restored below
+    frac_img += np.float32(0.5)
+    v_fr, r_fr = timed(lambda: sf.fit_batch(frac_img, None, out=outs, **call))
+    frac_img -= np.float32(0.5)
+    variants["pinned_fractional_no_inits"] = {
+        "value": v_fr, "unit": "fits/s", "h2d_bytes_per_step": h2d(r_fr), "d2h_bytes_per_step": d2h,
+        "chunks_u16_per_step": r_fr.stats.get("n_chunks_u16"),
+        "path": "fit_batch(pinned f32 images + 0.5): nothing narrows, f32 over PCIe (speed only, no parity)"}
     res["e2e_variants"] = variants
     return res
 
@@ -827,10 +842,11 @@ def c5_leg(sf, args, devs):
     fits = devs.sum(float(n))
     res = {"spots": int(fits), "n_gpus": devs.n_gpus, "value": fits * steps / s, "unit": "fits/s", "steps": steps,
            "s_per_step": s / steps, "scaling": "strong (fixed total of spots)",
-           "h2d_bytes_per_step": int(fits) * N * 4, "d2h_bytes_per_step": int(fits) * 26,
+           "h2d_bytes_per_step": int(devs.sum(float(r.stats.get("h2d_bytes") or 0))),
+           "input_bytes_per_step": int(fits) * N * 4, "d2h_bytes_per_step": int(fits) * 26,
            "path": "fit_batch(pinned numpy images, inits=None, out=pinned) -> sf_fit_batch(devices=all of this "
-                   "process): contiguous shards, one host thread per device, chunked H2D/kernel/D2H, fused "
-                   "initializer",
+                   "process): contiguous shards, one host thread per device, integer-valued chunks narrowed to "
+                   "u16 by the host, chunked H2D/kernel/D2H, initializer on the device",
            "chunks_per_step": r.stats.get("n_chunks"), "pinned_alloc_s": alloc_s, "generate_s": gen_s,
            "data": f"device simulator, seed {SEED}, global spot indices {lo}..{lo + n - 1} on rank {devs.rank}"}
     if note:

@@ -75,6 +75,8 @@ typedef struct sf_stats {
   double h2d_ms, kernel_ms, d2h_ms, total_ms; /* device-event times (summed over chunks / devices) */
   int32_t n_devices;
   int32_t n_chunks;
+  int32_t n_chunks_u16; /* host chunks that crossed PCIe as 16-bit counts (u16 input, or narrowed f32) */
+  uint64_t h2d_bytes;   /* bytes copied host -> device (pixels + inits), 0 for device-resident input */
 } sf_stats;
 
 /*

@@ -52,6 +52,8 @@ class sf_stats(ctypes.Structure):
         ("total_ms", ctypes.c_double),
         ("n_devices", ctypes.c_int32),
         ("n_chunks", ctypes.c_int32),
+        ("n_chunks_u16", ctypes.c_int32),
+        ("h2d_bytes", ctypes.c_uint64),
     ]
 
 

@@ -183,7 +183,7 @@ def fit_batch(images, inits=None, config: FitConfig = FitConfig(), engine: str =
                      _ptr(out.status), _ptr(out.iterations), dev_arr, len(devs), ctypes.byref(st)))
     out.stats = dict(n_gradient_evals=st.n_gradient_evals, n_trial_evals=st.n_trial_evals,
                      n_kernel_evals=st.n_kernel_evals, total_ms=st.total_ms, n_devices=st.n_devices,
-                     n_chunks=st.n_chunks)
+                     n_chunks=st.n_chunks, n_chunks_u16=st.n_chunks_u16, h2d_bytes=st.h2d_bytes)
     return out
 
 

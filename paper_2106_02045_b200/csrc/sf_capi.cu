@@ -350,6 +350,8 @@ struct HostJob {
   unsigned long long evals[3] = {0, 0, 0};
   double h2d_ms = 0, kernel_ms = 0, d2h_ms = 0;
   int chunks = 0;
+  int chunks_u16 = 0;
+  uint64_t h2d_bytes = 0;
   int rc = 0;
   std::string err;
 };
@@ -418,16 +420,19 @@ int run_shard(int dev, HostJob& j) {
   int64_t chunk = 0;
   for (const auto& ch : chunks) chunk = std::max(chunk, ch.second);
   const bool staging = !(j.pinned_in && j.pinned_out);
-  // Pageable f32 chunks whose pixels are all integers in [0, 65535] cross PCIe as u16
-  // (sf_host_narrow.cpp): the CPU has to touch pageable pixels anyway (staging copy), and narrowing
-  // writes half the bytes.  Pinned f32 input is not narrowed: its H2D is a DMA straight from the
-  // caller's buffer at ~53 GB/s, faster than the host narrows (~45 GB/s of input on 16 cores,
-  // profiles/r02_bench_e2e_narrow.txt).  SPOTFIT_NARROW=0 disables, =2 narrows pinned input as well.
+  // f32 chunks whose pixels are all integers in [0, 65535] cross PCIe as u16 (sf_host_narrow.cpp):
+  // the host narrows them into pinned staging with streaming stores, half the bytes cross PCIe and
+  // the fit kernel widens them back exactly.  Pageable input has to be staged by the CPU anyway;
+  // pinned input gains too, since the host narrows faster (~6.4e7 15x15 spots/s on 16 cores) than
+  // PCIe moves f32 (~5.9e7): profiles/r02_ab_narrow_pinned.txt.  The first chunk that does not narrow
+  // ends narrowing for the rest of the call (the pass gives up at its first bad value), so
+  // non-integer data costs one partial pass.  SPOTFIT_NARROW=0 disables, =1 narrows pageable input only.
   static const int narrow_env = [] {
     const char* e = std::getenv("SPOTFIT_NARROW");
-    return e ? (int)std::strtol(e, nullptr, 10) : 1;
+    return e ? (int)std::strtol(e, nullptr, 10) : 2;
   }();
   const bool narrow = narrow_env > 0 && !j.images16 && j.images != nullptr && (!j.pinned_in || narrow_env > 1);
+  bool narrow_live = narrow;  // cleared by the first chunk that does not narrow
   if (ensure_ctx(*c, dev, (size_t)chunk, N, P, staging, narrow) != 0) return -1;
   // reset the evaluation counters; the other slot streams wait on the device, not the host
   SF_CUDA(cudaMemsetAsync(c->d_evals, 0, 3 * sizeof(unsigned long long), c->slot[0].stream));
@@ -448,7 +453,8 @@ int run_shard(int dev, HostJob& j) {
     Slot& s = c->slot[ci % kStreams];
     const int64_t lo = j.lo + chunks[ci].first;
     const int64_t n = chunks[ci].second;
-    if (staging || narrow) {  // the slot's previous chunk must be finished before its staging is reused
+    const bool nar = narrow_live;
+    if (staging || nar) {  // the slot's previous chunk must be finished before its staging is reused
       SF_CUDA(cudaEventSynchronize(s.ev[3]));
       if (staging) copy_out_staged(s, j);
     }
@@ -456,7 +462,8 @@ int run_shard(int dev, HostJob& j) {
     SF_CUDA(mark(s.stream));
     // this chunk as u16: 16-bit input, or f32 input whose pixels all narrow exactly
     const bool u16 = j.images16 != nullptr ||
-                     (narrow && sf::par_narrow_u16(s.h_in16, j.images + lo * N, (size_t)(n * N), j.copy_threads));
+                     (nar && sf::par_narrow_u16(s.h_in16, j.images + lo * N, (size_t)(n * N), j.copy_threads));
+    if (nar && !u16) narrow_live = false;
     const size_t px_bytes = u16 ? sizeof(uint16_t) : sizeof(float);
     const void* src_img = j.images16 ? (const void*)(j.images16 + lo * N)
                                      : (u16 ? (const void*)s.h_in16 : (const void*)(j.images + lo * N));
@@ -476,6 +483,8 @@ int run_shard(int dev, HostJob& j) {
     // made the init copy wait behind the next chunks' pixel copies: tools/e2e_trace.py.)
     if (src_init)
       SF_CUDA(cudaMemcpyAsync(s.d_init, src_init, n * P * sizeof(float), cudaMemcpyHostToDevice, s.stream));
+    j.h2d_bytes += (uint64_t)n * N * px_bytes + (src_init ? (uint64_t)n * P * sizeof(float) : 0);
+    j.chunks_u16 += u16 ? 1 : 0;
     if (u16) {
       SF_CUDA(cudaMemcpyAsync(s.d_img16, src_img, n * N * px_bytes, cudaMemcpyHostToDevice, s.stream));
       SF_CUDA(mark(s.stream));
@@ -971,6 +980,8 @@ static int fit_batch_impl(const float* images, const uint16_t* images16, int32_t
       stats->n_trial_evals += j.evals[1];
       stats->n_kernel_evals += j.evals[2];
       stats->n_chunks += j.chunks;
+      stats->n_chunks_u16 += j.chunks_u16;
+      stats->h2d_bytes += j.h2d_bytes;
     }
     stats->n_devices = nd;
     stats->total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();

@@ -13,6 +13,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 #include <thread>
 #include <vector>
 
@@ -32,17 +33,25 @@ inline bool narrow_one(float v, uint16_t& out) {
   return (float)u == v;
 }
 
-bool narrow_scalar(uint16_t* dst, const float* src, size_t n) {
+// Every narrowing pass gives up as soon as it (or, through `stop`, another thread of the same chunk)
+// meets a value that does not narrow: the chunk then goes as f32 and the rest of the pass is wasted.
+constexpr size_t kCheck = 4096;  // elements between checks
+
+bool narrow_scalar(uint16_t* dst, const float* src, size_t n, std::atomic<bool>* stop) {
   bool ok = true;
-  for (size_t i = 0; i < n; ++i) ok &= narrow_one(src[i], dst[i]);
-  return ok;
+  for (size_t i = 0; i < n; ++i) {
+    ok &= narrow_one(src[i], dst[i]);
+    if ((i & (kCheck - 1)) == kCheck - 1 && (!ok || (stop && stop->load(std::memory_order_relaxed)))) break;
+  }
+  if (!ok && stop) stop->store(true, std::memory_order_relaxed);
+  return ok && !(stop && stop->load(std::memory_order_relaxed));
 }
 
 #ifndef SF_HOST_NT
 #define SF_HOST_NT 1  // streaming (non-temporal) stores into the pinned staging buffers
 #endif
 
-__attribute__((target("avx2"))) bool narrow_avx2(uint16_t* dst, const float* src, size_t n) {
+__attribute__((target("avx2"))) bool narrow_avx2(uint16_t* dst, const float* src, size_t n, std::atomic<bool>* stop) {
   const __m256i lim = _mm256_set1_epi32(0x477FFF00);
   __m256i bad = _mm256_setzero_si256();
   // A 32-byte aligned destination (the pinned staging buffer) takes streaming stores: the lines go
@@ -66,16 +75,23 @@ __attribute__((target("avx2"))) bool narrow_avx2(uint16_t* dst, const float* src
       _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i), p);
     else
       _mm256_storeu_si256(reinterpret_cast<__m256i*>(dst + i), p);
+    if (((i + 16) & (kCheck - 1)) == 0 &&
+        (!_mm256_testz_si256(bad, bad) || (stop && stop->load(std::memory_order_relaxed)))) {
+      if (nt) _mm_sfence();
+      if (stop) stop->store(true, std::memory_order_relaxed);
+      return false;
+    }
   }
   if (nt) _mm_sfence();
   bool ok = _mm256_testz_si256(bad, bad) != 0;
   for (; i < n; ++i) ok &= narrow_one(src[i], dst[i]);
+  if (!ok && stop) stop->store(true, std::memory_order_relaxed);
   return ok;
 }
 
-bool narrow_block(uint16_t* dst, const float* src, size_t n) {
+bool narrow_block(uint16_t* dst, const float* src, size_t n, std::atomic<bool>* stop) {
   static const bool avx2 = __builtin_cpu_supports("avx2");
-  return avx2 ? narrow_avx2(dst, src, n) : narrow_scalar(dst, src, n);
+  return avx2 ? narrow_avx2(dst, src, n, stop) : narrow_scalar(dst, src, n, stop);
 }
 
 // memcpy into a 32-byte aligned destination with streaming stores (the source unaligned)
@@ -131,17 +147,18 @@ void par_copy(void* dst, const void* src, size_t bytes, int threads) {
 bool par_narrow_u16(uint16_t* dst, const float* src, size_t n, int threads) {
   constexpr size_t kPiece = 1u << 20;  // elements
   const int T = (int)std::min<size_t>((size_t)std::max(1, threads), (n + kPiece - 1) / kPiece);
-  if (T <= 1) return narrow_block(dst, src, n);
+  std::atomic<bool> stop{false};
+  if (T <= 1) return narrow_block(dst, src, n, &stop);
   const size_t per = ((n + T - 1) / T + 15) & ~(size_t)15;
   std::vector<char> ok(T, 1);
   std::vector<std::thread> th;
   for (int t = 1; t < T; ++t) {
     const size_t a = std::min(n, per * t), b = std::min(n, per * (t + 1));
-    th.emplace_back([&, t, a, b] { ok[t] = narrow_block(dst + a, src + a, b - a); });
+    th.emplace_back([&, t, a, b] { ok[t] = narrow_block(dst + a, src + a, b - a, &stop); });
   }
-  ok[0] = narrow_block(dst, src, std::min(n, per));
+  ok[0] = narrow_block(dst, src, std::min(n, per), &stop);
   for (auto& x : th) x.join();
-  return std::all_of(ok.begin(), ok.end(), [](char c) { return c != 0; });
+  return !stop.load() && std::all_of(ok.begin(), ok.end(), [](char c) { return c != 0; });
 }
 
 }  // namespace sf

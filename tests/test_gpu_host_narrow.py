@@ -1,7 +1,8 @@
-"""The host pipeline's u16 narrowing of pageable f32 chunks (sf_capi.cu:run_shard, sf_host_narrow.cpp)
-never changes a result: batches of several chunks, all-integer or with single non-integer, negative,
--0.0 or > 65535 pixels in some chunks, fit bitwise like the same batch from pinned memory (which is
-never narrowed), with and without inits."""
+"""The host pipeline's u16 narrowing of f32 chunks (sf_capi.cu:run_shard, sf_host_narrow.cpp), for
+pageable and pinned input, never changes a result: batches of several chunks, all-integer or with
+single non-integer, negative, -0.0 or > 65535 pixels in some chunks, fit bitwise like the same batch
+resident on the device (no host pipeline), with and without inits.  The first chunk that does not
+narrow ends narrowing for the rest of the call (sf_stats.n_chunks_u16)."""
 import numpy as np
 import pytest
 
@@ -32,18 +33,34 @@ def _pinned_copy(a):
 
 
 @pytest.mark.parametrize("poison", [None, 0.5, -1.0, -0.0, 70000.0])
-def test_pageable_narrowing_is_invisible(sf, poison):
+@pytest.mark.parametrize("where", ["first", "middle"])
+def test_narrowing_is_invisible(sf, poison, where):
+    import torch
+
     W = H = 15
     count = 300_000  # several host chunks
+    if poison is None and where == "middle":
+        pytest.skip("same as first")
     im, _ = sf.simulate_batch(sf.SimConfig(width=W, height=H, count=count, seed=314))
     im = im.reshape(count, W * H)
     if poison is not None:
-        for s in (5, 150_001, count - 1):  # poison single pixels in the first, a middle and the last chunk
+        spots = (5, 150_001, count - 1) if where == "first" else (150_001,)
+        for s in spots:
             im[s, 17] = poison
-    pinned = _pinned_copy(im)
-    ref = sf.fit_batch(pinned, grid=sf.PixelGrid(W, H))  # pinned f32: never narrowed
-    got = sf.fit_batch(im, grid=sf.PixelGrid(W, H))      # pageable: narrowed where the chunk allows
-    _same(got, ref, f"poison={poison}")
-    ini, _ = sf.estimate_initial_batch(im[:20000], 3, grid=sf.PixelGrid(W, H))
-    _same(sf.fit_batch(im[:20000], ini, grid=sf.PixelGrid(W, H)),
-          sf.fit_batch(_pinned_copy(im[:20000]), ini, grid=sf.PixelGrid(W, H)), "with inits")
+    grid = sf.PixelGrid(W, H)
+    ref = sf.fit_batch(torch.from_numpy(im).cuda(), grid=grid)  # device-resident: no host pipeline
+    for label, src in (("pageable", im), ("pinned", _pinned_copy(im).numpy())):
+        got = sf.fit_batch(src, grid=grid)
+        _same(got, ref, f"{label} poison={poison} {where}")
+        n, n16 = got.stats["n_chunks"], got.stats["n_chunks_u16"]
+        if poison is None:
+            assert n16 == n and got.stats["h2d_bytes"] == count * W * H * 2, (label, got.stats)
+        elif where == "first":
+            assert n16 == 0, (label, got.stats)
+        else:
+            assert 0 < n16 < n, (label, got.stats)  # narrowed up to the poisoned chunk, f32 from there on
+    ini, _ = sf.estimate_initial_batch(im[:20000], 3, grid=grid)
+    ref_i = sf.fit_batch(torch.from_numpy(im[:20000]).cuda(), torch.from_numpy(ini).cuda(), grid=grid)
+    _same(sf.fit_batch(im[:20000], ini, grid=grid), ref_i, "pageable with inits")
+    _same(sf.fit_batch(_pinned_copy(im[:20000]).numpy(), _pinned_copy(ini).numpy(), grid=grid), ref_i,
+          "pinned with inits")
