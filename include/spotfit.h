@@ -88,7 +88,9 @@ typedef struct sf_stats {
  * streams; with n_devices > 1 the batch is split into contiguous shards, one
  * host thread per device, results written into disjoint slices.
  * out_params: [count][P]; out_alpha/out_beta/out_nchi2: [count]; out_status,
- * out_iters: [count] bytes.  stats may be NULL.
+ * out_iters: [count] bytes.  stats may be NULL.  Host f32 chunks whose pixels are all
+ * integers in [0, 65535] cross PCIe as u16, narrowed losslessly by the host (results unchanged;
+ * SPOTFIT_NARROW).
  */
 int sf_fit_batch(const float* images, int32_t width, int32_t height, int64_t count, const float* inits,
                  const sf_config* cfg, float* out_params, float* out_alpha, float* out_beta, float* out_nchi2,
