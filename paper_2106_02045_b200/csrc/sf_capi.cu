@@ -423,8 +423,7 @@ int run_shard(int dev, HostJob& j) {
   // f32 chunks whose pixels are all integers in [0, 65535] cross PCIe as u16 (sf_host_narrow.cpp):
   // the host narrows them into pinned staging with streaming stores, half the bytes cross PCIe and
   // the fit kernel widens them back exactly.  Pageable input has to be staged by the CPU anyway;
-  // pinned input gains too, since the host narrows faster (~6.4e7 15x15 spots/s on 16 cores) than
-  // PCIe moves f32 (~5.9e7): profiles/r02_ab_narrow_pinned.txt.  The first chunk that does not narrow
+  // for pinned input a share of the chunks is narrowed (below).  The first chunk that does not narrow
   // ends narrowing for the rest of the call (the pass gives up at its first bad value), so
   // non-integer data costs one partial pass.  SPOTFIT_NARROW=0 disables, =1 narrows pageable input only.
   static const int narrow_env = [] {
@@ -433,6 +432,19 @@ int run_shard(int dev, HostJob& j) {
   }();
   const bool narrow = narrow_env > 0 && !j.images16 && j.images != nullptr && (!j.pinned_in || narrow_env > 1);
   bool narrow_live = narrow;  // cleared by the first chunk that does not narrow
+  // Pinned input: every other chunk is narrowed (SPOTFIT_NARROW_PINNED percent, default 50; never
+  // the first).  The others go as f32 straight from the caller's buffer, so the copy engine moves
+  // them while the host narrows the next one: the host's narrowing rate and PCIe add up
+  // (profiles/r02_ab_narrow_pinned.txt: 7.1e7 15x15 fits/s vs 6.2e7 narrowing all, 5.9e7 none).
+  static const int pinned_pct = [] {
+    const char* e = std::getenv("SPOTFIT_NARROW_PINNED");
+    const long v = e ? std::strtol(e, nullptr, 10) : 50;
+    return (int)(v < 0 ? 0 : (v > 100 ? 100 : v));
+  }();
+  auto share = [&](size_t ci) {
+    return !j.pinned_in || pinned_pct >= 100 ||
+           (int64_t)(ci + 1) * pinned_pct / 100 > (int64_t)ci * pinned_pct / 100;
+  };
   if (ensure_ctx(*c, dev, (size_t)chunk, N, P, staging, narrow) != 0) return -1;
   // reset the evaluation counters; the other slot streams wait on the device, not the host
   SF_CUDA(cudaMemsetAsync(c->d_evals, 0, 3 * sizeof(unsigned long long), c->slot[0].stream));
@@ -453,7 +465,7 @@ int run_shard(int dev, HostJob& j) {
     Slot& s = c->slot[ci % kStreams];
     const int64_t lo = j.lo + chunks[ci].first;
     const int64_t n = chunks[ci].second;
-    const bool nar = narrow_live;
+    const bool nar = narrow_live && share(ci);
     if (staging || nar) {  // the slot's previous chunk must be finished before its staging is reused
       SF_CUDA(cudaEventSynchronize(s.ev[3]));
       if (staging) copy_out_staged(s, j);

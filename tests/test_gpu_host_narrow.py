@@ -2,7 +2,8 @@
 pageable and pinned input, never changes a result: batches of several chunks, all-integer or with
 single non-integer, negative, -0.0 or > 65535 pixels in some chunks, fit bitwise like the same batch
 resident on the device (no host pipeline), with and without inits.  The first chunk that does not
-narrow ends narrowing for the rest of the call (sf_stats.n_chunks_u16)."""
+narrow ends narrowing for the rest of the call; pinned input narrows a share of its chunks
+(sf_stats.n_chunks_u16, sf_stats.h2d_bytes)."""
 import numpy as np
 import pytest
 
@@ -52,9 +53,12 @@ def test_narrowing_is_invisible(sf, poison, where):
     for label, src in (("pageable", im), ("pinned", _pinned_copy(im).numpy())):
         got = sf.fit_batch(src, grid=grid)
         _same(got, ref, f"{label} poison={poison} {where}")
-        n, n16 = got.stats["n_chunks"], got.stats["n_chunks_u16"]
-        if poison is None:
-            assert n16 == n and got.stats["h2d_bytes"] == count * W * H * 2, (label, got.stats)
+        n, n16, nb = got.stats["n_chunks"], got.stats["n_chunks_u16"], got.stats["h2d_bytes"]
+        assert count * W * H * 2 <= nb <= count * W * H * 4, (label, got.stats)
+        if label == "pinned":  # a share of the chunks (never the first) is narrowed, the rest go as f32
+            assert (0 < n16 < n) if poison is None else (n16 < n), (label, got.stats)
+        elif poison is None:
+            assert n16 == n and nb == count * W * H * 2, (label, got.stats)
         elif where == "first":
             assert n16 == 0, (label, got.stats)
         else:
