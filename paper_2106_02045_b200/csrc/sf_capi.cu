@@ -199,7 +199,10 @@ int dispatch_eval(int P, const sf::LaunchEval& a) {
 // ---------------------------------------------------------------------------
 // Per-device context: streams, device chunk buffers, pinned staging, events.
 // ---------------------------------------------------------------------------
-constexpr int kStreams = 3;
+#ifndef SF_STREAMS
+#define SF_STREAMS 4  // chunk slots (stream + staging) per device: profiles/r02_ab_narrow_pinned.txt
+#endif
+constexpr int kStreams = SF_STREAMS;
 
 struct Slot {
   cudaStream_t stream = nullptr;
@@ -392,7 +395,7 @@ int run_shard(int dev, HostJob& j) {
   // Chunk schedule.  The host path is bound by the H2D copy engine (PCIe Gen5 x16: 53 GB/s at
   // 100 MB copies, 55.5 GB/s at 900 MB; tools/h2d_bw.py), so copies are large (<= 256 MB), and
   // the tail halves down to kMinChunk so that the kernel + D2H of the last chunk, which run
-  // after the final H2D, are short.  Three streams overlap H2D(k+1) with kernel(k).
+  // after the final H2D, are short.  Four streams overlap H2D(k+1) with kernel(k).
   const size_t px_bytes_in = j.images16 ? sizeof(uint16_t) : sizeof(float);
   // smallest chunk: total / 8 within [2048, 16384] spots, so that mid-size batches (1e4..1e5 spots)
   // still pipeline copy and fit over a few chunks (tools/call_overhead.py: 3e4 pageable spots
@@ -432,13 +435,13 @@ int run_shard(int dev, HostJob& j) {
   }();
   const bool narrow = narrow_env > 0 && !j.images16 && j.images != nullptr && (!j.pinned_in || narrow_env > 1);
   bool narrow_live = narrow;  // cleared by the first chunk that does not narrow
-  // Pinned input: every other chunk is narrowed (SPOTFIT_NARROW_PINNED percent, default 50; never
+  // Pinned input: three chunks in four are narrowed (SPOTFIT_NARROW_PINNED percent, default 75; never
   // the first).  The others go as f32 straight from the caller's buffer, so the copy engine moves
-  // them while the host narrows the next one: the host's narrowing rate and PCIe add up
-  // (profiles/r02_ab_narrow_pinned.txt: 7.1e7 15x15 fits/s vs 6.2e7 narrowing all, 5.9e7 none).
+  // them while the host narrows the next ones: the host's narrowing rate and PCIe add up
+  // (profiles/r02_ab_narrow_pinned.txt: 7.5e7 15x15 fits/s vs 6.2e7 narrowing all, 5.9e7 none).
   static const int pinned_pct = [] {
     const char* e = std::getenv("SPOTFIT_NARROW_PINNED");
-    const long v = e ? std::strtol(e, nullptr, 10) : 50;
+    const long v = e ? std::strtol(e, nullptr, 10) : 75;
     return (int)(v < 0 ? 0 : (v > 100 ? 100 : v));
   }();
   auto share = [&](size_t ci) {
