@@ -50,6 +50,9 @@ bool narrow_scalar(uint16_t* dst, const float* src, size_t n, std::atomic<bool>*
 #ifndef SF_HOST_NT
 #define SF_HOST_NT 1  // streaming (non-temporal) stores into the pinned staging buffers
 #endif
+#ifndef SF_HOST_PF
+#define SF_HOST_PF 256  // software prefetch distance in floats (1 KB; profiles/r02_ab_narrow_pinned.txt)
+#endif
 
 __attribute__((target("avx2"))) bool narrow_avx2(uint16_t* dst, const float* src, size_t n, std::atomic<bool>* stop) {
   const __m256i lim = _mm256_set1_epi32(0x477FFF00);
@@ -59,6 +62,7 @@ __attribute__((target("avx2"))) bool narrow_avx2(uint16_t* dst, const float* src
   const bool nt = SF_HOST_NT && ((uintptr_t)dst & 31) == 0;
   size_t i = 0;
   for (; i + 16 <= n; i += 16) {
+    if (SF_HOST_PF > 0) _mm_prefetch(reinterpret_cast<const char*>(src + i + SF_HOST_PF), _MM_HINT_T0);
     const __m256 v0 = _mm256_loadu_ps(src + i), v1 = _mm256_loadu_ps(src + i + 8);
     const __m256i b0 = _mm256_castps_si256(v0), b1 = _mm256_castps_si256(v1);
     // signed compare: sign-set patterns are negative (> lim fails, < 0 caught by the gt below)
@@ -100,6 +104,7 @@ __attribute__((target("avx2"))) void copy_nt_avx2(void* dst, const void* src, si
   const char* s = static_cast<const char*>(src);
   size_t i = 0;
   for (; i + 128 <= bytes; i += 128) {
+    if (SF_HOST_PF > 0) _mm_prefetch(s + i + 4 * SF_HOST_PF, _MM_HINT_T0);
     const __m256i a = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(s + i));
     const __m256i b = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(s + i + 32));
     const __m256i c = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(s + i + 64));
