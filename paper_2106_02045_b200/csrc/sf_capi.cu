@@ -438,7 +438,7 @@ int run_shard(int dev, HostJob& j) {
   // Pinned input: three chunks in four are narrowed (SPOTFIT_NARROW_PINNED percent, default 75; never
   // the first).  The others go as f32 straight from the caller's buffer, so the copy engine moves
   // them while the host narrows the next ones: the host's narrowing rate and PCIe add up
-  // (profiles/r02_ab_narrow_pinned.txt: 7.5e7 15x15 fits/s vs 6.2e7 narrowing all, 5.9e7 none).
+  // (profiles/r02_ab_narrow_pinned.txt: 7.7e7 15x15 fits/s vs 6.7-7.1e7 narrowing all, 5.9e7 none).
   static const int pinned_pct = [] {
     const char* e = std::getenv("SPOTFIT_NARROW_PINNED");
     const long v = e ? std::strtol(e, nullptr, 10) : 75;
