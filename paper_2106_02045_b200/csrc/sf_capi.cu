@@ -434,7 +434,8 @@ int run_shard(int dev, HostJob& j) {
     return e ? (int)std::strtol(e, nullptr, 10) : 2;
   }();
   const bool narrow = narrow_env > 0 && !j.images16 && j.images != nullptr && (!j.pinned_in || narrow_env > 1);
-  bool narrow_live = narrow;  // cleared by the first chunk that does not narrow
+  bool narrow_live = narrow;  // cleared by the first chunk that does not narrow (or narrows too slowly)
+  bool probed = false;        // pinned input: the first narrowed chunk's probe has run
   // Pinned input: three chunks in four are narrowed (SPOTFIT_NARROW_PINNED percent, default 75; never
   // the first).  The others go as f32 straight from the caller's buffer, so the copy engine moves
   // them while the host narrows the next ones: the host's narrowing rate and PCIe add up
@@ -476,9 +477,33 @@ int run_shard(int dev, HostJob& j) {
     SF_CUDA(cudaEventRecord(s.ev[0], s.stream));
     SF_CUDA(mark(s.stream));
     // this chunk as u16: 16-bit input, or f32 input whose pixels all narrow exactly
-    const bool u16 = j.images16 != nullptr ||
-                     (nar && sf::par_narrow_u16(s.h_in16, j.images + lo * N, (size_t)(n * N), j.copy_threads));
-    if (nar && !u16) narrow_live = false;
+    // Pinned input is narrowed only while the host keeps up: narrowing that runs slower than the f32
+    // bytes would cross PCIe (~50 GB/s, with 1.5x slack for the thread start-up) ends it for the call
+    // -- e.g. several processes or devices sharing the host's cores and memory bandwidth.  The call's
+    // first narrowed chunk is probed on its first half, so a slow host gives up after a partial pass
+    // and sends the chunk as f32.
+    auto narrow_part = [&](int64_t a, int64_t m, bool guard) -> int {  // 1 narrowed, 0 not integer, -1 too slow
+      const auto t0 = std::chrono::steady_clock::now();
+      if (!sf::par_narrow_u16(s.h_in16 + a * N, j.images + (lo + a) * N, (size_t)(m * N), j.copy_threads)) return 0;
+      const double t = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      return guard && t > 1.5 * (double)m * N * sizeof(float) / 50e9 ? -1 : 1;
+    };
+    bool u16 = j.images16 != nullptr;
+    if (nar) {
+      int r = 1;
+      if (j.pinned_in && !probed) {
+        probed = true;
+        const int64_t m = std::max<int64_t>(1, n / 2);
+        const int r0 = narrow_part(0, m, true);
+        if (r0 == 1 && m < n) r = narrow_part(m, n - m, true);
+        u16 = r0 == 1 && r != 0;  // a slow probe leaves the rest un-narrowed: the chunk goes as f32
+        if (r0 != 1 || r != 1) narrow_live = false;
+      } else {
+        r = narrow_part(0, n, j.pinned_in);
+        u16 = r != 0;  // narrowed (a slow pass still counts for this chunk, not for the next ones)
+        if (r != 1) narrow_live = false;
+      }
+    }
     const size_t px_bytes = u16 ? sizeof(uint16_t) : sizeof(float);
     const void* src_img = j.images16 ? (const void*)(j.images16 + lo * N)
                                      : (u16 ? (const void*)s.h_in16 : (const void*)(j.images + lo * N));
