@@ -43,6 +43,23 @@ def test_version_and_struct_layout(L):
     assert ctypes.sizeof(_lib.sf_config) == 8 + 11 * 8
 
 
+def test_ctypes_structs_mirror_the_header():
+    """Every C struct of include/spotfit.h and its ctypes mirror in _lib.py: same field names in the
+    same order (the ABI the reference-side binding in INTEGRATION.md relies on)."""
+    from paper_2106_02045_b200 import _lib
+
+    hdr = open(os.path.join(ROOT, "include", "spotfit.h")).read()
+    hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
+    for name in ("sf_stats", "sf_config"):
+        body = re.search(r"typedef struct %s \{(.*?)\} %s;" % (name, name), hdr, re.S).group(1)
+        fields = []
+        for decl in body.split(";"):
+            decl = decl.strip()
+            if decl:
+                fields += [f.strip() for f in re.sub(r"^[\w\s]*?\b(?:u?int\d+_t|double|float|int)\b", "", decl).split(",")]
+        assert [f for f, _ in getattr(_lib, name)._fields_] == fields, name
+
+
 def test_lane_geometry_reproduces_numpy_pairwise_order(L):
     """Emulate the kernel's reduction (chain lanes -> xor 1,2,4 -> leaf tails ->
     slot butterfly -> 0.0 +) with the C++ lane geometry and compare with
