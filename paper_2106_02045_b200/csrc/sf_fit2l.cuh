@@ -22,6 +22,15 @@
 #pragma once
 #include "sf_fit_kernel.cuh"
 
+#ifndef SF_2L_U1
+#define SF_2L_U1 1  // pass-1 pair loop unroll (A/B knob)
+#endif
+#ifndef SF_2L_U2
+#define SF_2L_U2 1  // pass-2 pair loop unroll (A/B knob)
+#endif
+#define SF_STR_(x) #x
+#define SF_UNROLL(n) _Pragma(SF_STR_(unroll n))
+
 namespace sf {
 namespace l2 {
 
@@ -203,7 +212,7 @@ __device__ __forceinline__ void chain1_2l(Smem<SL, P>& S, const Lane& L, int v, 
   float2* f3p = S.f3 + v * S.np * TPB + tid;      // P = 4
   const float4* xyp = S.xy + vl;                  // pair i: xyp[VL i] (coordinate table)
   uint32_t tc = L.tw + (uint32_t)(v * S.np * 8);  // pair i: column tc + 8 i
-#pragma unroll 1
+  SF_UNROLL(SF_2L_U1)
   for (int i = 0; i < S.np; ++i, gp += TPB, f3p += TPB, tc += 8, xyp += Smem<SL, P>::VL) {
     f2 cx, cy, f, fg[P], t[Q1];
     pair_xy2l<SL, P>(xyp, L, v, i, nz, cx, cy);
@@ -249,7 +258,7 @@ __device__ __forceinline__ void chain2_2l(Smem<SL, P>& S, const Lane& L, int v, 
   const float2* gp = S.g + v * S.np * TPB + tid;
   const float2* f3p = S.f3 + v * S.np * TPB + tid;
   uint32_t tc = L.tw + (uint32_t)(v * S.np * 8);
-#pragma unroll 1
+  SF_UNROLL(SF_2L_U2)
   for (int i = 0; i < S.np; ++i, gp += TPB, f3p += TPB, tc += 8) {
     f2 f, fg[P], t[Q2];
     tm_ld8(tc, f, fg[0], fg[1], fg[2]);
