@@ -306,10 +306,16 @@ int sf_shard_range(int64_t count, int32_t shard, int32_t n_shards, int64_t* lo, 
 /*
  * sf_debug_narrow_u16 -- diagnostic: the host pipeline's lossless narrowing of f32 pixel chunks for
  * the PCIe leg (sf_fit_batch sends a pageable f32 chunk as u16 when every pixel is an integer in
- * [0, 65535] with a clear sign bit; SPOTFIT_NARROW=0 disables it, =2 applies it to pinned input too).  Returns 1 if all n values narrowed (dst
+ * [0, 65535] with a clear sign bit; SPOTFIT_NARROW).  Returns 1 if all n values narrowed (dst
  * holds them), 0 if some value did not, -1 on bad arguments.  Host-only.
  */
 int sf_debug_narrow_u16(const float* src, int64_t n, uint16_t* dst, int32_t threads);
+
+/*
+ * sf_debug_par_copy -- diagnostic: the host pipeline's staging copy of pageable input (threads,
+ * streaming stores into a 32-byte aligned destination).  Returns 0, or -1 on bad arguments.  Host-only.
+ */
+int sf_debug_par_copy(void* dst, const void* src, int64_t bytes, int32_t threads);
 
 int sf_device_count(void);
 const char* sf_last_error(void);

@@ -134,6 +134,7 @@ SYMBOLS = {
     "sf_csv_last_error": (ctypes.c_char_p, []),
     "sf_shard_range": (ctypes.c_int, [_i64, _i32, _i32, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]),
     "sf_debug_narrow_u16": (ctypes.c_int, [_vp, _i64, _vp, _i32]),
+    "sf_debug_par_copy": (ctypes.c_int, [_vp, _vp, _i64, _i32]),
     "sf_host_alloc": (ctypes.c_void_p, [ctypes.c_size_t]),
     "sf_host_free": (None, [_vp]),
     "sf_device_count": (ctypes.c_int, []),

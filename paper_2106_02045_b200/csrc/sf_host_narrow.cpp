@@ -172,3 +172,9 @@ extern "C" int sf_debug_narrow_u16(const float* src, int64_t n, uint16_t* dst, i
   if (n < 0 || (n > 0 && (!src || !dst))) return -1;
   return sf::par_narrow_u16(dst, src, (size_t)n, threads) ? 1 : 0;
 }
+
+extern "C" int sf_debug_par_copy(void* dst, const void* src, int64_t bytes, int32_t threads) {
+  if (bytes < 0 || (bytes > 0 && (!src || !dst))) return -1;
+  sf::par_copy(dst, src, (size_t)bytes, threads);
+  return 0;
+}
