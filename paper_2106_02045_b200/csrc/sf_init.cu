@@ -554,12 +554,12 @@ __device__ __forceinline__ int count_contig(const PX* sp, int N, double thr, int
   return m;
 }
 
-template <int L, typename PX, bool QUAD>
-__global__ void __launch_bounds__(32 * init_warps<QUAD>(), init_minb<QUAD>()) init_kernel(const PX* __restrict__ images, int W, int H,
+template <int L, typename PX, bool QUAD, bool SMALL = QUAD>
+__global__ void __launch_bounds__(32 * init_warps<SMALL>(), init_minb<SMALL>()) init_kernel(const PX* __restrict__ images, int W, int H,
                                                               int64_t count, int P, double smin, double smax,
                                                               float* __restrict__ inits, float* __restrict__ amps) {
   constexpr int G = 32 / L;
-  constexpr int kInitWarps = init_warps<QUAD>();  // (shadows the default for this instantiation)
+  constexpr int kInitWarps = init_warps<SMALL>();  // (shadows the default for this instantiation)
   extern __shared__ __align__(16) unsigned char init_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int sub = lane / L, sl = lane % L;  // spot of the warp's G, lane within the spot
@@ -748,16 +748,16 @@ __global__ void __launch_bounds__(32 * init_warps<QUAD>(), init_minb<QUAD>()) in
 #endif
 }
 
-template <int L, typename PX, bool QUAD = false>
+template <int L, typename PX, bool QUAD = false, bool SMALL = QUAD>
 cudaError_t launch_init_l(const PX* images, int W, int H, int64_t count, int P, double smin, double smax,
                           float* inits, float* amps, cudaStream_t stream) {
   constexpr int G = 32 / L;
-  constexpr int kInitWarps = init_warps<QUAD>();
+  constexpr int kInitWarps = init_warps<SMALL>();
   // staging buffers (<= 66 KB) + the sigma(M) table
   const size_t smem = ((16 + (size_t)kInitWarps * 2 * init_buf_elems<PX>(G, W * H) * sizeof(PX) +
                        (size_t)(W * H + 1) * sizeof(float) + 7) & ~(size_t)7) +
                      (size_t)kInitWarps * 2 * sizeof(uint64_t);
-  auto kern = init_kernel<L, PX, QUAD>;
+  auto kern = init_kernel<L, PX, QUAD, SMALL>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, per_sm = 0;
@@ -790,8 +790,20 @@ cudaError_t launch_init_px(const PX* images, int W, int H, int64_t count, int P,
       if (W > 16 && W <= 32 && N <= 512)
         return launch_init_l<8, PX, true>(images, W, H, count, P, sigma_min, sigma_max, inits, amps, stream);
     }
-  if (W <= 16 && N <= 256) return launch_init_l<8, PX>(images, W, H, count, P, sigma_min, sigma_max, inits, amps, stream);
-  if (W <= 32 && N <= 512) return launch_init_l<16, PX>(images, W, H, count, P, sigma_min, sigma_max, inits, amps, stream);
+#ifndef SF_INIT_SMALLPAIR
+#define SF_INIT_SMALLPAIR 0
+#endif
+  if (W <= 16 && N <= 256)
+    return launch_init_l<8, PX, false, SF_INIT_SMALLPAIR>(images, W, H, count, P, sigma_min, sigma_max, inits, amps, stream);
+  if (W <= 32 && N <= 512)
+    return launch_init_l<16, PX, false, SF_INIT_SMALLPAIR>(images, W, H, count, P, sigma_min, sigma_max, inits, amps, stream);
+#ifndef SF_INIT_BIGPAIR
+#define SF_INIT_BIGPAIR 1
+#endif
+  // 16 < W <= 32 with N up to 1024 (32x32): adjacent pairs on 16 lanes, 2 spots per warp, in small CTAs
+  // (3 warps) so that the 8 KB staging windows still leave 12 warps per SM
+  if (SF_INIT_BIGPAIR && W > 16 && W <= 32 && N <= 1024)
+    return launch_init_l<16, PX, false, true>(images, W, H, count, P, sigma_min, sigma_max, inits, amps, stream);
   return launch_init_l<32, PX>(images, W, H, count, P, sigma_min, sigma_max, inits, amps, stream);
 }
 
