@@ -781,15 +781,17 @@ cudaError_t launch_init_px(const PX* images, int W, int H, int64_t count, int P,
   // L lanes per spot, G = 32 / L spots per warp: the fewest lanes that leave each lane at most two
   // columns (W <= 2L) with G * N <= 1024 pixels per warp buffer; more spots per warp share the
   // per-spot reductions and bookkeeping
-  if constexpr (sizeof(PX) == 4 && SF_INIT_QUAD)
-    // odd N only: the 8 spots of a warp start an odd number of words apart, which spreads their
-    // lanes' shared loads over the banks (an even N such as 16x16 lines them up: 8-way conflicts)
-    if (N & 1) {
-      if (W > 8 && W <= 16 && N <= 256)
-        return launch_init_l<4, PX, true>(images, W, H, count, P, sigma_min, sigma_max, inits, amps, stream);
-      if (W > 16 && W <= 32 && N <= 512)
-        return launch_init_l<8, PX, true>(images, W, H, count, P, sigma_min, sigma_max, inits, amps, stream);
-    }
+#ifndef SF_INIT_QUAD8_EVEN
+#define SF_INIT_QUAD8_EVEN 1  // widths 17..32: the quad walk for even N too (2-way bank conflicts at most, still faster)
+#endif
+  if constexpr (sizeof(PX) == 4 && SF_INIT_QUAD) {  // f32 pixels only (walk_quad_f32)
+    // widths 9..16: odd N only -- the 8 spots of a warp then start an odd number of words apart, which
+    // spreads their lanes' shared loads over the banks (an even N such as 16x16 lines them up: 8-way)
+    if ((N & 1) && W > 8 && W <= 16 && N <= 256)
+      return launch_init_l<4, PX, true>(images, W, H, count, P, sigma_min, sigma_max, inits, amps, stream);
+    if ((N & 1 || SF_INIT_QUAD8_EVEN) && W > 16 && W <= 32 && N <= 512)
+      return launch_init_l<8, PX, true>(images, W, H, count, P, sigma_min, sigma_max, inits, amps, stream);
+  }
 #ifndef SF_INIT_SMALLPAIR
 #define SF_INIT_SMALLPAIR 0
 #endif

@@ -44,7 +44,7 @@ for W, H in ((15, 15), (21, 21), (32, 32)):
 # the standalone initializer on every geometry family of its column walk (one column per lane, several
 # row segments per column, a 1-row grid, a wide grid with several columns per lane) and on non-integer
 # pixels (general path), against the oracle; the fused initializer (inits = None) and the model functions
-for W, H in ((15, 15), (5, 9), (1, 7), (9, 1), (40, 1), (13, 10), (32, 32), (11, 11), (21, 21), (16, 3), (13, 13), (9, 2), (15, 3), (17, 5), (25, 3), (27, 27), (20, 30)):
+for W, H in ((15, 15), (5, 9), (1, 7), (9, 1), (40, 1), (13, 10), (32, 32), (11, 11), (21, 21), (16, 3), (13, 13), (9, 2), (15, 3), (17, 5), (25, 3), (27, 27), (20, 30), (20, 20), (18, 7)):
     im, _ = sf.simulate_batch(sf.SimConfig(width=W, height=H, count=37, seed=W + 7 * H))
     im = im.reshape(37, -1)
     im[5] += 0.25  # one non-tame spot
